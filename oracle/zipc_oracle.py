@@ -1,0 +1,455 @@
+"""fp64 CPU oracle of the Zipage compression step (TEST INFRASTRUCTURE ONLY).
+
+Every function cites the passage of /root/reference/PAPER.md (arXiv 2603.08743)
+it follows, as ``PAPER.md:<line> (<section / Alg / Eq>)``. Where the paper is
+silent or garbled, the reading taken is the numbered one of SURVEY.md §8(c),
+restated in DESIGN.md §Readings as R1..R17.
+
+Data conventions (plain numpy; nothing here imports the CUDA product):
+  * K, V pools: arrays [L, N_total, b, h_kv, d] of raw element bits —
+    ``np.uint16`` for bf16 (bf16 bits), ``np.float32`` for fp32.
+  * Q window cache: [L, M, w, h_q, d], same element type; row u of slot j is
+    the query of position T-w+u (R3).
+  * block tables: int32 [R, stride]; seq_lens int32 [R]; budgets int32 [R, L, h_kv].
+  * free stack: int32 [capacity] with valid entries [0, top); pop takes
+    stack[top-1].
+All floating-point arithmetic is fp64 on exactly-widened inputs.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+# Status codes (same numeric values the C-ABI documents; restated here, not
+# imported, so that the oracle shares nothing with the product).
+OK = 0
+ERR_NOT_TRIGGERED = -10
+ERR_BAD_TABLE = -11
+ERR_BAD_BUDGET = -12
+ERR_NO_FREE_BLOCKS = -13
+ERR_SEQ_TOO_LONG = -14
+ERR_BAD_SLOT = -15
+ERR_CAPACITY = -16
+
+F_PREFIX = 1
+F_VALIDATE = 2
+
+
+@dataclass
+class Geometry:
+    """Pool geometry, PAPER.md:42 (§3 'Pre-allocated memory') and :69 (§4.2, Q cache)."""
+    L: int
+    h_kv: int
+    h_q: int
+    d: int
+    b: int
+    N_total: int
+    M: int
+    w: int
+    dtype: str  # "bf16" | "fp32"
+
+    @property
+    def G(self) -> int:
+        return self.h_q // self.h_kv
+
+
+@dataclass
+class Params:
+    n_max: int
+    pool_kernel: int = 1
+    max_seq_len: int = 1 << 30
+    flags: int = 0
+
+
+# --------------------------------------------------------------------------
+# element widening (exact)
+# --------------------------------------------------------------------------
+def widen(x: np.ndarray, dtype: str) -> np.ndarray:
+    """Exact widening of stored elements to fp64. bf16 bits -> fp32 -> fp64 is exact."""
+    if dtype == "bf16":
+        return (x.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    if dtype == "fp32":
+        return x.astype(np.float64)
+    raise ValueError(dtype)
+
+
+# --------------------------------------------------------------------------
+# a0: validate and plan targets — PAPER.md:61-66 (§4.1), :131-138 (§4.5)
+# --------------------------------------------------------------------------
+@dataclass
+class Plan:
+    status: int
+    n_blocks: np.ndarray = field(default=None)   # N per request
+    n_prefix: np.ndarray = field(default=None)   # shared leading blocks (R11)
+    targets: np.ndarray = field(default=None)    # [R, n_max-1] physical ids
+    reserved: np.ndarray = field(default=None)   # [R]
+    fresh: list = field(default=None)            # per request: fresh ids in pop order
+
+
+def _request_error(geo, prm, r, seq_lens, tables, table_stride, budgets, ref_counts, q_slots):
+    """Per-request checks in the fixed order of DESIGN.md §Errors. Returns (err, N, n_prefix)."""
+    T = int(seq_lens[r])
+    if q_slots is not None and not (0 <= int(q_slots[r]) < geo.M):
+        return ERR_BAD_SLOT, 0, 0
+    if T > prm.max_seq_len:
+        return ERR_SEQ_TOO_LONG, 0, 0
+    N = -(-T // geo.b)  # ceil(T/b): blocks occupied
+    if N > table_stride:
+        return ERR_BAD_TABLE, N, 0
+    # trigger: N >= N_max (R14 allows a partial last block)
+    if N < prm.n_max:
+        return ERR_NOT_TRIGGERED, N, 0
+    row = [int(x) for x in tables[r, :N]]
+    if any(bid < 0 or bid >= geo.N_total for bid in row):
+        return ERR_BAD_TABLE, N, 0
+    if (prm.flags & F_VALIDATE) and len(set(row)) != len(row):
+        return ERR_BAD_TABLE, N, 0
+    n_prefix = 0
+    if prm.flags & F_PREFIX:
+        # shared = reference count > 1; R11: must be a leading run
+        while n_prefix < N and ref_counts[row[n_prefix]] > 1:
+            n_prefix += 1
+        if any(ref_counts[bid] > 1 for bid in row[n_prefix:]):
+            return ERR_BAD_TABLE, N, n_prefix
+    kmax = (prm.n_max - 1) * geo.b  # k = (N_max-1)*b
+    bud = budgets[r]
+    if np.any(bud < geo.w) or np.any(bud > kmax):
+        return ERR_BAD_BUDGET, N, n_prefix
+    return OK, N, n_prefix
+
+
+def plan(geo: Geometry, prm: Params, seq_lens, tables, budgets, ref_counts=None,
+         free_stack=None, free_top=0, q_slots=None, free_capacity=None, freed_capacity=None) -> Plan:
+    """Trigger check, prefix-aware target choice (§4.5 bullets), fresh pops.
+
+    Targets (R9, R10): N_prefix = 0 -> own table[0..N_max-2] (Fig. 1: "moved to the
+    first three blocks"). N_prefix >= N_max-1 -> N_max-1 fresh blocks
+    (PAPER.md:134). Otherwise fresh for j < N_prefix, own table[j] for j >= N_prefix
+    (PAPER.md:135). Reserved = own table[max(N_prefix, N_max-1)], or one more fresh
+    pop when the table is wholly shared. Fresh blocks pop from the free-stack top
+    in (request, target index) order, the reserved pop last.
+    """
+    R = len(seq_lens)
+    table_stride = tables.shape[1] if R else 0
+    nb = np.zeros(R, np.int64)
+    npf = np.zeros(R, np.int64)
+    for r in range(R):
+        err, N, n_prefix = _request_error(geo, prm, r, seq_lens, tables, table_stride,
+                                          budgets, ref_counts, q_slots)
+        if err != OK:
+            return Plan(status=err)
+        nb[r], npf[r] = N, n_prefix
+    nm1 = prm.n_max - 1
+    targets = np.zeros((R, nm1), np.int32)
+    reserved = np.zeros(R, np.int32)
+    fresh_lists = []
+    top = int(free_top)
+    # demand check before any pop (all-or-nothing)
+    demand = 0
+    for r in range(R):
+        n_fresh = min(int(npf[r]), nm1)
+        res_idx = max(int(npf[r]), nm1)
+        demand += n_fresh + (1 if res_idx >= nb[r] else 0)
+    if demand > top:
+        return Plan(status=ERR_NO_FREE_BLOCKS)
+    if freed_capacity is not None or free_capacity is not None:
+        priv = sum(max(0, int(nb[r]) - 1 - max(int(npf[r]), nm1)) for r in range(R))
+        shared_entries = int(sum(npf))
+        if freed_capacity is not None and priv + shared_entries > freed_capacity:
+            return Plan(status=ERR_CAPACITY)
+        if free_capacity is not None and top - demand + priv + shared_entries > free_capacity:
+            return Plan(status=ERR_CAPACITY)
+    for r in range(R):
+        N, n_prefix = int(nb[r]), int(npf[r])
+        row = tables[r]
+        fr = []
+        for j in range(nm1):
+            if j < n_prefix:  # fresh target (j < min(N_prefix, N_max-1))
+                top -= 1
+                targets[r, j] = free_stack[top]
+                fr.append(int(targets[r, j]))
+            else:             # reuse own block at the same logical index
+                targets[r, j] = row[j]
+        res_idx = max(n_prefix, nm1)
+        if res_idx < N:
+            reserved[r] = row[res_idx]
+        else:
+            top -= 1
+            reserved[r] = free_stack[top]
+            fr.append(int(reserved[r]))
+        fresh_lists.append(fr)
+    return Plan(status=OK, n_blocks=nb, n_prefix=npf, targets=targets, reserved=reserved,
+                fresh=fresh_lists)
+
+
+# --------------------------------------------------------------------------
+# a1: window-query x key logits — Alg. 1, PAPER.md:369-405 (§C.2)
+# --------------------------------------------------------------------------
+def _group(geo: Geometry, h: int):
+    """R5: query head i uses KV head floor(i/G) -> group of KV head h = [h*G, h*G+G)."""
+    return range(h * geo.G, (h + 1) * geo.G)
+
+
+def logits_blockwise(geo: Geometry, q_slot_l: np.ndarray, k_layer: np.ndarray, table, T: int, h: int,
+                     ) -> np.ndarray:
+    """Formulation A: Alg. 1 block by block.
+
+    q_slot_l: [w, h_q, d] fp64 (one layer, one query slot); k_layer: [N_total, b, h_kv, d] fp64.
+    Returns A: [G, w, N*b] fp64 with -inf at masked / out-of-sequence entries.
+    A'[u, v] = Q_j K_i^T / sqrt(d). Mask (R1, R2): window row u is
+    position p_u = T-w+u; entry t is masked iff t > p_u; slots t >= T are not tokens.
+    """
+    w, b, d = geo.w, geo.b, geo.d
+    N = -(-T // b)
+    out = np.full((geo.G, w, N * b), -np.inf)
+    for gi, g in enumerate(_group(geo, h)):
+        Qj = q_slot_l[:, g, :]                       # [w, d]  (Alg.1 line 2)
+        for i in range(N):                           # parallel over blocks
+            Ki = k_layer[table[i], :, h, :]          # [b, d]  (Alg.1 lines 3-5)
+            Ap = (Qj @ Ki.T) / math.sqrt(d)          # [w, b]  (Alg.1 line 6)
+            for u in range(w):
+                for v in range(b):
+                    t = i * b + v
+                    if t >= T or t > T - w + u:
+                        Ap[u, v] = -np.inf
+            out[gi, :, i * b:(i + 1) * b] = Ap       # A[i] <- A' (Alg.1 line 11)
+    return out
+
+
+def logits_dense(geo: Geometry, q_slot_l: np.ndarray, k_layer: np.ndarray, table, T: int, h: int
+                 ) -> np.ndarray:
+    """Formulation B: gather K densely into [T, d], one matrix product per query head.
+    Returns [G, w, T] with -inf where t > T-w+u."""
+    b = geo.b
+    t = np.arange(T)
+    Kd = k_layer[np.asarray(table)[t // b], t % b, h, :]       # [T, d]
+    out = np.empty((geo.G, geo.w, T))
+    for gi, g in enumerate(_group(geo, h)):
+        out[gi] = (q_slot_l[:, g, :] @ Kd.T) / math.sqrt(geo.d)
+    u = np.arange(geo.w)[:, None]
+    mask = t[None, :] > (T - geo.w + u)
+    out[:, mask] = -np.inf
+    return out
+
+
+# --------------------------------------------------------------------------
+# a2: softmax over the window row, GQA max, mean over window — PAPER.md:409-411
+# --------------------------------------------------------------------------
+def attention_scores(A: np.ndarray, T: int) -> np.ndarray:
+    """A: [G, w, >=T] logits with -inf masks. Reshape to w x (N b) and softmax along
+    the last dim, max-reduce over the query heads of the KV group,
+    then mean over the w window rows. Returns s: [T] fp64."""
+    A = A[:, :, :T]
+    m = A.max(axis=2, keepdims=True)
+    E = np.exp(A - m)                      # exp(-inf) = 0 for masked entries
+    P = E / E.sum(axis=2, keepdims=True)   # softmax per (g, u)
+    return P.max(axis=0).mean(axis=0)      # max over g, then mean over u
+
+
+def unit_scores(geo: Geometry, q_cache_f64, k_pool_f64, table, T: int, slot: int, l: int, h: int,
+                blockwise: bool = False) -> np.ndarray:
+    """S for one unit (request, layer, KV head) from widened caches."""
+    q = q_cache_f64[l, slot]           # [w, h_q, d]
+    kl = k_pool_f64[l]                 # [N_total, b, h_kv, d]
+    A = (logits_blockwise if blockwise else logits_dense)(geo, q, kl, table, T, h)
+    return attention_scores(A, T)
+
+
+# --------------------------------------------------------------------------
+# a3: MaxPool1D and window pin — PAPER.md:480-487 (§C.4), :85, :591
+# --------------------------------------------------------------------------
+def max_pool(s: np.ndarray, k: int) -> np.ndarray:
+    """S = MaxPool1D(S); R6: odd kernel, stride 1, same length,
+    out-of-range neighbours ignored."""
+    if k == 1:
+        return s.copy()
+    r = k // 2
+    T = len(s)
+    return np.array([s[max(0, t - r):min(T, t + r + 1)].max() for t in range(T)])
+
+
+def pin_window(s: np.ndarray, T: int, w: int) -> np.ndarray:
+    """Entries of the observation window get +inf."""
+    out = s.copy()
+    out[T - w:T] = np.inf
+    return out
+
+
+# --------------------------------------------------------------------------
+# a4: per-head top-l with the index tie rule — PAPER.md:85, :591 (§C.6)
+# --------------------------------------------------------------------------
+def select(s_final: np.ndarray, ell: int) -> np.ndarray:
+    """Keep the ell positions first under (score desc, position desc) (R7), ascending."""
+    T = len(s_final)
+    order = np.lexsort((np.arange(T), s_final))   # ascending by score, then position
+    kept = order[T - ell:]
+    return np.sort(kept).astype(np.int32)
+
+
+def kept_to_tag(kept: np.ndarray, N: int, b: int) -> np.ndarray:
+    """Top-k tag T in {0,1}^{N x b}."""
+    tag = np.zeros(N * b, np.int8)
+    tag[kept] = 1
+    return tag.reshape(N, b)
+
+
+# --------------------------------------------------------------------------
+# a5: compaction — Alg. 4
+# --------------------------------------------------------------------------
+def compact_alg4(k_layer: np.ndarray, v_layer: np.ndarray, table, targets, tag: np.ndarray, h: int, b: int):
+    """Formulation A: the two-pointer sweep of Alg. 4, literally (in place).
+
+    Read pointer p_r walks the request's logical slots block by block through the
+    table; write pointer p_w walks the target sequence (targets[0..N_max-2], R9/R10).
+    k_layer/v_layer: [N_total, b, h_kv, d] raw element arrays of ONE layer.
+    """
+    N = tag.shape[0]
+    pr = (0, 0)      # (logical block i, slot)   Alg.4 line 1
+    pw = (0, 0)      # (target index, slot)
+    ell, s, i = 0, 0, 0                                           # line 2
+    while i < N:                                                  # line 3
+        if tag[i][ell % b] == 1:                                  # line 4
+            kvec = k_layer[table[pr[0]], pr[1], h, :].copy()      # line 5
+            vvec = v_layer[table[pr[0]], pr[1], h, :].copy()      # line 6
+            k_layer[targets[pw[0]], pw[1], h, :] = kvec           # line 7
+            v_layer[targets[pw[0]], pw[1], h, :] = vvec           # line 8
+            s += 1                                                # line 9
+            pw = (pw[0] + 1, 0) if s % b == 0 else (pw[0], pw[1] + 1)   # lines 10-14
+        ell += 1                                                  # line 16
+        if ell % b == 0:                                          # line 17
+            pr = (pr[0] + 1, 0)
+            i += 1
+        else:
+            pr = (pr[0], pr[1] + 1)
+
+
+def compact_gather(k_layer, v_layer, table, targets, kept: np.ndarray, h: int, b: int):
+    """Formulation B: snapshot the kept rows first, then write new[rank] = old[kept[rank]]."""
+    table = np.asarray(table)
+    targets = np.asarray(targets)
+    src_blk, src_slot = table[kept // b], kept % b
+    ks = k_layer[src_blk, src_slot, h, :].copy()
+    vs = v_layer[src_blk, src_slot, h, :].copy()
+    rank = np.arange(len(kept))
+    k_layer[targets[rank // b], rank % b, h, :] = ks
+    v_layer[targets[rank // b], rank % b, h, :] = vs
+
+
+# --------------------------------------------------------------------------
+# a6: tables, ref counts, freed list — PAPER.md:64 (§4.1), :138 (§4.5); Fig. 1 caption :22
+# --------------------------------------------------------------------------
+@dataclass
+class FinalizeOut:
+    tables: np.ndarray
+    new_num_blocks: np.ndarray
+    freed: np.ndarray
+    free_stack: np.ndarray
+    free_top: int
+    ref_counts: np.ndarray | None
+
+
+def finalize(geo: Geometry, prm: Params, pl: Plan, tables, ref_counts, free_stack, free_top) -> FinalizeOut:
+    """New table = targets ++ [reserved] (N_max entries; the N_max-th block is reserved
+    for decoding). Freed = each request's private blocks that are neither
+    targets nor reserved, ascending logical index, requests in input order; then the
+    shared blocks whose count this call drove to 0, ascending id. Shared blocks get
+    ref -= 1. With ref counts: fresh targets/reserved -> 1, freed private -> 0.
+    The freed list is pushed onto the free stack in list order."""
+    R = len(pl.n_blocks)
+    nm1 = prm.n_max - 1
+    tables = tables.copy()
+    refs = None if ref_counts is None else ref_counts.copy()
+    stack = free_stack.copy()
+    top = int(free_top) - sum(len(f) for f in pl.fresh)
+    freed = []
+    zeroed = set()
+    for r in range(R):
+        N, n_prefix = int(pl.n_blocks[r]), int(pl.n_prefix[r])
+        old = [int(x) for x in tables[r, :N]]
+        first_priv_free = max(n_prefix, nm1) + 1
+        for j in range(first_priv_free, N):
+            freed.append(old[j])
+            if refs is not None:
+                refs[old[j]] = 0
+        if refs is not None:
+            for j in range(n_prefix):
+                refs[old[j]] -= 1
+                if refs[old[j]] == 0:
+                    zeroed.add(old[j])
+            for bid in pl.fresh[r]:
+                refs[bid] = 1
+        tables[r, :nm1] = pl.targets[r]
+        tables[r, nm1] = pl.reserved[r]
+    freed.extend(sorted(zeroed))
+    for bid in freed:
+        stack[top] = bid
+        top += 1
+    return FinalizeOut(tables=tables, new_num_blocks=np.full(R, prm.n_max, np.int32),
+                       freed=np.asarray(freed, np.int32), free_stack=stack, free_top=top,
+                       ref_counts=refs)
+
+
+# --------------------------------------------------------------------------
+# the whole step
+# --------------------------------------------------------------------------
+@dataclass
+class CompressOut:
+    status: int
+    k_cache: np.ndarray = None
+    v_cache: np.ndarray = None
+    new_lens: np.ndarray = None      # [R, L, h_kv]
+    kept: dict = None                # (r, l, h) -> ascending kept positions
+    scores: dict = None              # (r, l, h) -> raw s (pre-pool) fp64
+    fin: FinalizeOut = None
+    plan: Plan = None
+
+
+def compress(geo: Geometry, prm: Params, k_cache, v_cache, q_cache, q_slots, seq_lens, tables, budgets,
+             ref_counts=None, free_stack=None, free_top=0, kept_override=None, blockwise=False,
+             free_capacity=None, freed_capacity=None, units=None) -> CompressOut:
+    """Steps 1-9 of SURVEY.md §8(c) for every request r (input order), layer l, KV head h.
+
+    kept_override: optional dict (r, l, h) -> kept list, used to drive compaction with
+    a kept set chosen elsewhere (the 'bytes' parity rule). units: optional subset of
+    (r, l, h) to score (for sampled checks); compaction then needs kept_override.
+    """
+    pl = plan(geo, prm, seq_lens, tables, budgets, ref_counts, free_stack, free_top, q_slots,
+              free_capacity, freed_capacity)
+    if pl.status != OK:
+        return CompressOut(status=pl.status, plan=pl)
+    R = len(seq_lens)
+    k_out = k_cache.copy()
+    v_out = v_cache.copy()
+    qf = widen(q_cache, geo.dtype)
+    kf = widen(k_cache, geo.dtype)
+    new_lens = np.zeros((R, geo.L, geo.h_kv), np.int32)
+    kept_all, scores = {}, {}
+    for r in range(R):
+        T = int(seq_lens[r])
+        for l in range(geo.L):
+            for h in range(geo.h_kv):
+                ell = min(T, int(budgets[r, l, h]))
+                new_lens[r, l, h] = ell
+                key = (r, l, h)
+                if kept_override is not None and key in kept_override:
+                    kept = np.asarray(kept_override[key], np.int32)
+                else:
+                    if units is not None and key not in units:
+                        continue
+                    s = unit_scores(geo, qf, kf, tables[r], T, int(q_slots[r]), l, h, blockwise)
+                    scores[key] = s
+                    kept = select(pin_window(max_pool(s, prm.pool_kernel), T, geo.w), ell)
+                kept_all[key] = kept
+    for r in range(R):
+        N = int(pl.n_blocks[r])
+        for l in range(geo.L):
+            for h in range(geo.h_kv):
+                key = (r, l, h)
+                if key not in kept_all:
+                    continue
+                compact_gather(k_out[l], v_out[l], tables[r], pl.targets[r], kept_all[key], h, geo.b)
+    fin = finalize(geo, prm, pl, tables, ref_counts, free_stack, free_top)
+    return CompressOut(status=OK, k_cache=k_out, v_cache=v_out, new_lens=new_lens, kept=kept_all,
+                       scores=scores, fin=fin, plan=pl)
