@@ -1,0 +1,397 @@
+#!/usr/bin/env python
+"""Benchmark of the Zipage compression step (BASELINE.json metric: requests compressed/s and
+fraction of HBM peak), one process per GPU, requests sharded by rank (weak scaling).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config qwen7b] [--impl zipc|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+A step = one zpc_compress call over the per-GPU batch (configs[1]: 64 requests x 8192 tokens,
+Qwen2.5-7B shape) — all stages a0..a6. Between steps the modified part of the pool is restored
+from a pristine copy (untimed, on the same stream; it also writes > L2 so L2 is flushed); each
+step is timed with CUDA events on the launching stream; the job time is the max over ranks.
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM_GBS = 6650.0
+FALLBACK_BF16_TFLOPS = 1590.0
+
+
+def load_peaks():
+    try:
+        p = json.load(open(PEAKS_PATH))
+        return dict(hbm=float(p["hbm_gbs"]), bf16=float(p["bf16_tflops"]),
+                    bf16_sust=float(p.get("bf16_tflops_sustained", p["bf16_tflops"])), src="measured")
+    except Exception:
+        return dict(hbm=FALLBACK_HBM_GBS, bf16=FALLBACK_BF16_TFLOPS, bf16_sust=1400.0, src="fallback")
+
+
+# ---------------------------------------------------------------- clocks sampler
+THROTTLE_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+                 0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+                 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+
+class ClockSampler:
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.samples = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+        except Exception:
+            self.proc = None
+            return
+
+        def read():
+            for line in self.proc.stdout:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) == 3:
+                    try:
+                        self.samples.append((float(parts[0]), float(parts[1]), int(parts[2], 16)))
+                    except ValueError:
+                        pass
+        self.thread = threading.Thread(target=read, daemon=True)
+        self.thread.start()
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        if not self.samples:
+            return None
+        busy = [s for s in self.samples if not (s[2] & 0x1)] or self.samples
+        reasons = set()
+        for s in busy:
+            for bit, name in THROTTLE_BITS.items():
+                if s[2] & bit and name != "gpu_idle":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(s[0] for s in busy), "sm_max_mhz": max(s[1] for s in busy),
+                "reasons": sorted(reasons), "samples": len(busy)}
+
+
+# ---------------------------------------------------------------- oracle (CPU baseline / reference arm)
+def oracle_sample(cfg, seed, rids, n_req):
+    """Host inputs for n_req sampled requests, as a compact sub-pool (untimed preparation)."""
+    from zpc_inputs import make_host_workload, scaled
+    sub = scaled(cfg, seq_lens=[cfg.seq_lens[int(r)] for r in rids[:n_req]], free_slack=8)
+    return make_host_workload(sub, seed, rids=np.arange(n_req))
+
+
+_ORACLE_CACHE = {}
+
+
+def time_oracle(cfg, seed, n_req, budget_s=20.0):
+    """Time the oracle (as it stands) on a bounded sample: whole requests restricted to a layer
+    subset (the oracle's cost is per (layer, head) unit; req/s is scaled by units per request)."""
+    import oracle as O
+    import torch
+    from zpc_inputs import scaled
+    threads = torch.get_num_threads()
+    key = (cfg.name, seed, n_req)
+    if key not in _ORACLE_CACHE:
+        sub = scaled(cfg, L=min(cfg.L, 2))
+        hw = oracle_sample(sub, seed, np.arange(max(1, n_req)), max(1, n_req))
+        _ORACLE_CACHE[key] = (sub, hw)
+    sub, hw = _ORACLE_CACHE[key]
+    lay = hw.layout
+    geo = O.Geometry(L=sub.L, h_kv=sub.h_kv, h_q=sub.h_q, d=sub.d, b=sub.b, N_total=lay.N_total, M=lay.M,
+                     w=sub.w, dtype=sub.dtype)
+    prm = O.Params(n_max=sub.n_max, pool_kernel=sub.pool_kernel,
+                   flags=O.F_PREFIX if lay.ref_counts is not None else 0)
+    units_done = 0
+    t0 = time.perf_counter()
+    while True:
+        out = O.compress(geo, prm, hw.k_cache, hw.v_cache, hw.q_cache, lay.q_slots, lay.seq_lens, lay.tables,
+                         hw.budgets, lay.ref_counts, lay.free_stack, lay.free_top)
+        assert out.status == O.OK
+        units_done += len(lay.seq_lens) * sub.L * sub.h_kv
+        el = time.perf_counter() - t0
+        if el >= budget_s:
+            break
+    units_per_req = cfg.L * cfg.h_kv
+    req_per_s = units_done / units_per_req / el
+    return req_per_s, dict(units=units_done, seconds=el, threads=threads,
+                           sample=f"{len(lay.seq_lens)} request(s) x {sub.L} of {cfg.L} layers x {cfg.h_kv} heads, "
+                                  f"T={int(lay.seq_lens[0])}, repeated {units_done // (sub.L * sub.h_kv)}x; "
+                                  f"req/s = units/s / {units_per_req} units per request")
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+# ---------------------------------------------------------------- GPU arm
+def algorithmic_bytes(cfg, seq_lens, budgets, moves):
+    """SURVEY §8(d) per-unit algorithmic bytes summed over the batch."""
+    e = 2 if cfg.dtype == "bf16" else 4
+    T = np.asarray(seq_lens, np.int64)
+    units_per_req = cfg.L * cfg.h_kv
+    score = int((T * cfg.d * e + cfg.G * cfg.w * cfg.d * e + 4 * T).sum() * units_per_req)
+    ell = np.minimum(np.asarray(budgets, np.int64), T[:, None, None])
+    select = int((4 * T).sum() * units_per_req + 4 * ell.sum())
+    compact = int(4 * moves * cfg.d * e)
+    flops_score = int(2 * cfg.G * cfg.w * cfg.d * T.sum() * units_per_req)
+    return dict(score=score, select=select, compact=compact, flops_score=flops_score)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="qwen7b")
+    ap.add_argument("--impl", default="zipc", choices=["zipc", "reference"])
+    ap.add_argument("--seed", type=int, default=2603)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cudacore", action="store_true", help="force the CUDA-core scoring kernel")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    from zpc_inputs import CONFIGS
+    cfg = CONFIGS[args.config]
+    per_gpu = cfg.wave or cfg.R
+    workload = (f"{cfg.name}: {per_gpu} req/GPU x {cfg.seq_lens[0]} tok, L={cfg.L} h_kv={cfg.h_kv} h_q={cfg.h_q} "
+                f"d={cfg.d} b={cfg.b} w={cfg.w} N_max={cfg.n_max} budget={cfg.budget} pool={cfg.pool_kernel}"
+                + (f" prefix={cfg.prefix_tokens}" if cfg.prefix_tokens else ""))
+
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        steps = []
+        info = None
+        for _ in range(args.warmup):
+            time_oracle(cfg, args.seed, 1, budget_s=0.5)
+        for _ in range(args.steps):
+            v, info = time_oracle(cfg, args.seed, 1, budget_s=3.0)
+            steps.append(v)
+        value = float(np.mean(steps))
+        line = {"impl": "reference", "metric": "requests_compressed_per_s", "value": value, "unit": "req/s",
+                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": 1000.0 / value if value else None, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic (zpc_inputs Philox recipe)",
+                "config": {"workload": workload},
+                "cpu_baseline": {"value": value, "unit": "req/s", "cores": info["threads"], "kind": "oracle",
+                                 "sample": info["sample"], "cpu": cpu_model()},
+                "e2e": {"value": value, "unit": "req/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return 0
+
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+
+    from paper_2603_08743_b200 import zipc
+    from paper_2603_08743_b200.batch import batch_of, desc_params
+    from zpc_inputs.device import generate
+
+    rids = np.arange(rank * per_gpu, (rank + 1) * per_gpu) % cfg.R
+    w = generate(cfg, args.seed, rids, device=dev)
+    flags = zipc.ZPC_F_COUNT_MOVES | (zipc.ZPC_F_SCORE_CUDACORE if args.cudacore else 0)
+    desc, params = desc_params(w, flags=flags)
+    batch = batch_of(w, desc, params)
+    stream = torch.cuda.current_stream()
+    lay = w.layout
+    nm = cfg.n_max
+    # pristine copies of everything a step mutates
+    touched = np.unique(np.concatenate([lay.tables[:, :nm].ravel(), lay.free_stack[:lay.free_top]]))
+    touched = touched[touched >= 0]
+    touched_d = torch.from_numpy(touched.astype(np.int64)).to(dev)
+    k0 = w.k.index_select(1, touched_d)
+    v0 = w.v.index_select(1, touched_d)
+    state0 = {n: getattr(w, n).clone() for n in ("tables", "free_stack", "free_top")}
+    refs0 = None if w.ref_counts is None else w.ref_counts.clone()
+
+    def restore():
+        w.k.index_copy_(1, touched_d, k0)
+        w.v.index_copy_(1, touched_d, v0)
+        for n, t in state0.items():
+            getattr(w, n).copy_(t)
+        if refs0 is not None:
+            w.ref_counts.copy_(refs0)
+
+    stages = [zipc.zpc_plan, zipc.zpc_score, zipc.zpc_select, zipc.zpc_compact, zipc.zpc_finalize]
+    stage_names = ["plan", "score", "select", "compact", "finalize"]
+
+    def step(evs):
+        evs[0].record(stream)
+        for i, fn in enumerate(stages):
+            fn(desc, params, batch, stream)
+            evs[i + 1].record(stream)
+
+    mk = lambda: [torch.cuda.Event(enable_timing=True) for _ in range(len(stages) + 1)]  # noqa: E731
+    for _ in range(max(3, args.warmup)):
+        restore()
+        step(mk())
+    torch.cuda.synchronize()
+    assert int(w.status.item()) == 0, zipc.status_string(int(w.status.item()))
+    moves = int(w.workspace[zipc.zpc_workspace_layout_get(desc, params, len(rids)).moves:][:8].view(torch.int64).item())
+
+    sampler = ClockSampler(local if world > 1 else torch.cuda.current_device())
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    time.sleep(0.3)
+    all_evs = []
+    wall0 = time.perf_counter()
+    for _ in range(args.steps):
+        restore()
+        evs = mk()
+        step(evs)
+        all_evs.append(evs)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - wall0
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    stage_ms = np.zeros(len(stages))
+    for evs in all_evs:
+        for i in range(len(stages)):
+            stage_ms[i] += evs[i].elapsed_time(evs[i + 1])
+    step_ms_total = float(stage_ms.sum())
+    t = torch.tensor([step_ms_total], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    max_ms = float(t.item())
+    R_all = per_gpu * world
+    ms_per_step = max_ms / args.steps
+    value = R_all / (ms_per_step / 1000.0)
+    T_sum = int(lay.seq_lens.sum())
+
+    peaks = load_peaks()
+    ab = algorithmic_bytes(cfg, lay.seq_lens, w.budgets_host, moves)
+    score_ms = stage_ms[1] / args.steps
+    compact_ms = stage_ms[3] / args.steps
+    step_bytes = ab["score"] + ab["select"] + ab["compact"]
+    roofline = {"kernel": "score (a1+a2)", "bound": "hbm", "achieved": ab["score"] / (score_ms / 1e3) / 1e9,
+                "peak": peaks["hbm"], "unit": "GB/s", "peak_src": peaks["src"], "traffic": None,
+                "algorithmic_bytes_per_launch": ab["score"]}
+    roofline["frac"] = roofline["achieved"] / roofline["peak"]
+    tensor_tf = ab["flops_score"] * 2 / (score_ms / 1e3) / 1e12   # two passes of 2*G*w*d per token
+    extra = {
+        "stage_ms": {n: round(float(x) / args.steps, 4) for n, x in zip(stage_names, stage_ms)},
+        "score_tensor_tflops_two_pass": tensor_tf,
+        "compact_roofline": {"achieved": ab["compact"] / (compact_ms / 1e3) / 1e9 if compact_ms else None,
+                             "peak": peaks["hbm"], "unit": "GB/s", "moved_rows": moves,
+                             "frac": (ab["compact"] / (compact_ms / 1e3) / 1e9) / peaks["hbm"] if compact_ms else None},
+        "step_hbm_frac": step_bytes / (ms_per_step / 1e3) / 1e9 / peaks["hbm"],
+        "kv_tokens_per_s": T_sum * world / (ms_per_step / 1e3),
+        "wall_s_incl_restores": wall,
+    }
+
+    # ---- e2e: host bookkeeping through zpc_compress_host (H2D + step + D2H every step)
+    e2e = None
+    if not args.no_e2e:
+        host = {n: getattr(w, n).cpu().pin_memory() for n in ("q_slots", "seq_lens", "budgets", "new_lens",
+                                                            "new_num_blocks", "freed", "num_freed", "status")}
+        host_t0 = {n: state0[n].cpu().pin_memory() for n in ("tables", "free_stack", "free_top")}
+        host_live = {n: t.clone().pin_memory() for n, t in host_t0.items()}
+        href = None if refs0 is None else refs0.cpu().pin_memory()
+        href_live = None if href is None else href.clone().pin_memory()
+        need = zipc.zpc_workspace_bytes_host(desc, params, len(rids), lay.table_stride, lay.N_total,
+                                             int(w.freed.numel()))
+        ws_h = torch.empty(need, dtype=torch.uint8, device=dev)
+        hb = zipc.make_batch(k_cache=w.k, v_cache=w.v, q_cache=w.q, q_slots=host["q_slots"],
+                             seq_lens=host["seq_lens"], block_tables=host_live["tables"], budgets=host["budgets"],
+                             new_lens=host["new_lens"], new_num_blocks=host["new_num_blocks"], ref_counts=href_live,
+                             free_stack=host_live["free_stack"], free_top=host_live["free_top"],
+                             freed_blocks=host["freed"], num_freed=host["num_freed"], workspace=ws_h,
+                             status=host["status"])
+        R = len(rids)
+        h2d = 4 * (R * 2 + R * lay.table_stride + host["budgets"].numel() + lay.N_total + 1) + \
+            (4 * lay.N_total if href is not None else 0)
+        d2h = 4 * (R * lay.table_stride + host["new_lens"].numel() + R + lay.N_total + int(w.freed.numel()) + 3) + \
+            (4 * lay.N_total if href is not None else 0)
+        e2e_ms = 0.0
+        for i in range(max(3, args.warmup) + args.steps):
+            restore()
+            for n in host_live:
+                host_live[n].copy_(host_t0[n])
+            if href_live is not None:
+                href_live.copy_(href)
+            torch.cuda.synchronize()
+            a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            zipc.zpc_compress_host(desc, params, hb, stream)
+            b_.record(stream)
+            b_.synchronize()
+            assert int(host["status"][0]) == 0
+            if i >= max(3, args.warmup):
+                e2e_ms += a.elapsed_time(b_)
+        te = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": R_all / (float(te.item()) / args.steps / 1e3), "unit": "req/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "path": "zpc_compress_host: block tables, budgets, free stack, ref counts host-resident (pinned); "
+                       "K/V/Q caches device-resident (the paged pool lives in HBM)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v_cpu, info = time_oracle(cfg, args.seed, 1, budget_s=15.0)
+        cpu = {"value": v_cpu, "unit": "req/s", "cores": info["threads"], "kind": "oracle",
+               "sample": info["sample"], "cpu": cpu_model(), "seconds": info["seconds"]}
+
+    launches_per_step = 2 + 2 + 1 + 1 + 2   # plan(2) score(lse+final) select compact finalize(2)
+    if rank == 0:
+        line = {"metric": "requests_compressed_per_s", "value": value, "unit": "req/s", "n_gpus": world,
+                "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_per_step,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": cfg.dtype,
+                "data": "synthetic (zpc_inputs Philox recipe, generated in HBM)",
+                "config": {"workload": workload, "requests_per_gpu": per_gpu,
+                           "l2": "pool > L2 (15 GB K for qwen7b); modified blocks restored from a pristine copy "
+                                 "between steps (untimed, writes > L2)",
+                           "parallelism": f"request-sharded x{world}, no data-path collective"},
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": launches_per_step * args.steps, "clocks": clocks, **extra}
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

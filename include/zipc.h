@@ -1,0 +1,192 @@
+/*
+ * zipc.h — C ABI of the B200-native compression step of Compressed PagedAttention
+ * (Zipage, arXiv 2603.08743). Library: paper_2603_08743_b200/lib/libzipc.so (sm_100a).
+ *
+ * What one call computes (PAPER.md = /root/reference/PAPER.md):
+ *   For every request r flagged for compression, every layer l and KV head h (a "unit"):
+ *   a0 plan      trigger check N >= N_max (§4.1); prefix-aware target blocks
+ *                (§4.5); fresh blocks popped from the free stack.
+ *   a1 score     logits q.k/sqrt(d) of the last w window queries against every cached key,
+ *                read through the block table, causal in absolute positions (Alg. 1,
+ *                PAPER.md:369-405).
+ *   a2           softmax over each window row, max over the GQA group, mean over the window
+ *                  ->  S[t], fp32.
+ *   a3 select    MaxPool1D along the sequence, window pinned to +inf
+ *                (PAPER.md:85, :591),
+ *   a4           keep the top min(T, budget) tokens per head, ties -> later position,
+ *                emitted in ascending order.
+ *   a5 compact   move kept K/V rows, in order, into the target blocks (Alg. 4).
+ *   a6 finalize  new table = targets ++ [reserved]; freed list; ref counts; free-stack push
+ *                (PAPER.md:22, :64, :138).
+ *   The readings taken where the paper is silent or garbled are DESIGN.md §Readings R1..R17.
+ *
+ * Conventions for every entry point:
+ *   - All array pointers are caller-owned DEVICE memory unless the name says _host.
+ *     The library allocates nothing, keeps no global state, never synchronises the stream.
+ *     Outputs are valid after the caller synchronises `stream` (a cudaStream_t; NULL = legacy).
+ *   - Host-detectable errors (bad descriptor/params, workspace too small) return a negative
+ *     ZPC_ERR_* and enqueue NOTHING.
+ *   - Device-detected errors are written to *status (device int32) by the plan stage; every
+ *     later stage reads *status at entry and returns without touching memory if it is non-zero.
+ *     All-or-nothing: plan checks everything before any mutation.
+ *   - Determinism: outputs are bit-identical run to run and independent of how requests are
+ *     sharded across GPUs (all per-request quantities; free-list order is defined below).
+ *   - Concurrency: two calls may run on different streams only if they share no allocator
+ *     (free stack / ref counts), no workspace and no request.
+ */
+#ifndef ZIPC_H_
+#define ZIPC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ZPC_ABI_VERSION 1
+
+/* ---- return / status codes ---- */
+#define ZPC_OK                  0
+#define ZPC_ERR_INVALID_ARG    -1   /* bad descriptor/params: even pool_kernel, w<1, n_max<2,
+                                       unsupported head_dim/dtype, h_q not a multiple of h_kv,
+                                       G*w > 256, max_seq_len above the select limit, NULL pointer */
+#define ZPC_ERR_WORKSPACE      -2   /* workspace_bytes < zpc_workspace_bytes(...) */
+#define ZPC_ERR_CUDA           -3   /* a launch failed (cudaGetLastError) */
+#define ZPC_ERR_NOT_TRIGGERED -10   /* device: N = ceil(T/b) < N_max */
+#define ZPC_ERR_BAD_TABLE     -11   /* device: N > table_stride, block id out of [0,N_total),
+                                       duplicate id (ZPC_F_VALIDATE), or a shared block
+                                       (ref > 1) after a private one (ZPC_F_PREFIX) */
+#define ZPC_ERR_BAD_BUDGET    -12   /* device: budget outside [w, (N_max-1)*b] */
+#define ZPC_ERR_NO_FREE_BLOCKS -13  /* device: free stack holds fewer blocks than the fresh
+                                       targets/reserved blocks the plan needs */
+#define ZPC_ERR_SEQ_TOO_LONG  -14   /* device: seq_len > params.max_seq_len */
+#define ZPC_ERR_BAD_SLOT      -15   /* device: q_slot outside [0, M) */
+#define ZPC_ERR_CAPACITY      -16   /* device: freed list or free stack would overflow */
+/* When several requests fail, *status is the error of the lowest-index failing request
+ * (its first failing check in the order SLOT, SEQ_TOO_LONG, TABLE(stride), NOT_TRIGGERED,
+ * TABLE(range), TABLE(dup), TABLE(prefix run), BUDGET); batch-level checks come after. */
+
+/* ---- element type of K, V and Q (one type for all three) ---- */
+#define ZPC_BF16 0
+#define ZPC_FP32 1
+
+/* ---- flags ---- */
+#define ZPC_F_PREFIX      1u  /* use ref_counts: leading blocks with ref > 1 are shared (§4.5) */
+#define ZPC_F_VALIDATE    2u  /* also reject duplicate block ids inside a table */
+#define ZPC_F_COUNT_MOVES 4u  /* count moved rows into the workspace counter (bytes accounting) */
+#define ZPC_F_SCORE_CUDACORE 8u /* force the CUDA-core scoring kernel even for bf16 (testing) */
+
+/* Pool geometry: K, V [L][N_total][b][h_kv][d], Q [L][M][w][h_q][d].
+ * Q row u of slot j holds the query of position T-w+u of the request bound to slot j (R3). */
+typedef struct {
+  int32_t num_layers;    /* L */
+  int32_t num_kv_heads;  /* h_kv */
+  int32_t num_q_heads;   /* h_q, a multiple of h_kv; query head i uses KV head i / (h_q/h_kv) (R5) */
+  int32_t head_dim;      /* d: 64 or 128 */
+  int32_t block_size;    /* b >= 1 */
+  int32_t num_blocks;    /* N_total */
+  int32_t num_q_slots;   /* M */
+  int32_t window;        /* w >= 1 (may exceed b) */
+  int32_t dtype;         /* ZPC_BF16 or ZPC_FP32 */
+} zpc_cache_desc;
+
+typedef struct {
+  int32_t n_max;         /* N_max >= 2: blocks per request after compression */
+  int32_t pool_kernel;   /* 1 = no pooling; odd >= 3 = MaxPool1D width, stride 1, same length (R6) */
+  int32_t max_seq_len;   /* host bound on seq_lens: sizes the workspace and grids (<= ZPC_MAX_SEQ_LEN) */
+  uint32_t flags;        /* ZPC_F_* */
+} zpc_params;
+
+#define ZPC_MAX_SEQ_LEN 49152   /* select keeps a unit's scores in shared memory */
+
+/* Everything one call touches. Pointers are device memory. Layouts:
+ *   q_slots      int32 [R]                 query slot of each request
+ *   seq_lens     int32 [R]                 T_r; N_r = ceil(T_r / b) blocks are in use
+ *   block_tables int32 [R][table_stride]   in/out: first N_max entries rewritten
+ *   budgets      int32 [R][L][h_kv]        per-head budget, w <= budget <= (N_max-1)*b
+ *   new_lens     int32 [R][L][h_kv]  out   kept entries per head = min(T_r, budget) (R8)
+ *   new_num_blocks int32 [R]         out   = N_max
+ *   ref_counts   int32 [N_total] in/out    or NULL (then ZPC_F_PREFIX must be clear)
+ *   free_stack   int32 [free_capacity]     valid entries [0, *free_top); pop = stack[top-1]
+ *   freed_blocks int32 [freed_capacity] out, *num_freed out:
+ *                private blocks that are neither targets nor reserved, ascending logical
+ *                index, requests in input order; then shared blocks this call drove to ref 0,
+ *                ascending id. They are also pushed onto the free stack in that order.
+ *   status       int32 [1] out             ZPC_OK or a device ZPC_ERR_*
+ */
+typedef struct {
+  void* k_cache;
+  void* v_cache;
+  const void* q_cache;
+  int32_t num_requests;
+  const int32_t* q_slots;
+  const int32_t* seq_lens;
+  int32_t* block_tables;
+  int32_t table_stride;
+  const int32_t* budgets;
+  int32_t* new_lens;
+  int32_t* new_num_blocks;
+  int32_t* ref_counts;
+  int32_t* free_stack;
+  int32_t* free_top;
+  int32_t free_capacity;
+  int32_t* freed_blocks;
+  int32_t* num_freed;
+  int32_t freed_capacity;
+  void* workspace;          /* device scratch, >= zpc_workspace_bytes(...), 256-B aligned */
+  size_t workspace_bytes;
+  int32_t* status;
+} zpc_batch;
+
+/* Where intermediate results live inside the workspace (byte offsets; all 256-B aligned). */
+typedef struct {
+  size_t total_bytes;
+  size_t scores;     /* fp32 [R][L][h_kv][max_seq_len]: S before pooling/pinning (a2 output) */
+  size_t kept;       /* int32 [R][L][h_kv][kept_stride]: ascending kept positions (a4 output) */
+  size_t targets;    /* int32 [R][N_max-1]: physical target block of each rank/b (a0 output) */
+  size_t reserved;   /* int32 [R] */
+  size_t n_prefix;   /* int32 [R] */
+  size_t lse;        /* fp32 [R][L][h_kv][G*w]: log2-domain log-sum-exp per window row/head */
+  size_t moves;      /* unsigned long long [1]: rows moved (ZPC_F_COUNT_MOVES) */
+  size_t internal;   /* library-private scratch */
+  int32_t kept_stride;   /* (N_max-1)*b */
+} zpc_workspace_layout;
+
+/* Workspace size for R requests; 0 if the descriptor/params are invalid. */
+size_t zpc_workspace_bytes(const zpc_cache_desc* desc, const zpc_params* params, int32_t num_requests);
+int zpc_workspace_layout_get(const zpc_cache_desc* desc, const zpc_params* params, int32_t num_requests,
+                             zpc_workspace_layout* out);
+
+/* The whole step a0..a6, stream-ordered, no host sync. */
+int zpc_compress(const zpc_cache_desc* desc, const zpc_params* params, const zpc_batch* batch, void* stream);
+
+/* Stage entry points (same conventions; each consumes the previous stage's workspace output).
+ * zpc_plan writes *status, targets/reserved/n_prefix and the internal scan; it mutates nothing
+ * outside the workspace and *status. zpc_score writes S and LSE. zpc_select writes kept and
+ * new_lens. zpc_compact moves K/V rows. zpc_finalize rewrites tables, ref counts, freed list,
+ * free stack and top, new_num_blocks. */
+int zpc_plan(const zpc_cache_desc* desc, const zpc_params* params, const zpc_batch* batch, void* stream);
+int zpc_score(const zpc_cache_desc* desc, const zpc_params* params, const zpc_batch* batch, void* stream);
+int zpc_select(const zpc_cache_desc* desc, const zpc_params* params, const zpc_batch* batch, void* stream);
+int zpc_compact(const zpc_cache_desc* desc, const zpc_params* params, const zpc_batch* batch, void* stream);
+int zpc_finalize(const zpc_cache_desc* desc, const zpc_params* params, const zpc_batch* batch, void* stream);
+
+/* End-to-end variant for host-resident bookkeeping (the e2e benchmark path): `host` holds the
+ * same fields, but q_slots, seq_lens, block_tables, budgets, new_lens, new_num_blocks,
+ * ref_counts, free_stack, free_top, freed_blocks, num_freed and status point to HOST memory
+ * (pinned for async copies); k_cache, v_cache, q_cache and workspace are device memory.
+ * The call stages the host inputs into the workspace (H2D), runs zpc_compress, and copies every
+ * output back (D2H), all on `stream`. Host buffers must stay alive until the stream is synced.
+ * Workspace must be >= zpc_workspace_bytes_host(...). */
+size_t zpc_workspace_bytes_host(const zpc_cache_desc* desc, const zpc_params* params, int32_t num_requests,
+                                int32_t table_stride, int32_t free_capacity, int32_t freed_capacity);
+int zpc_compress_host(const zpc_cache_desc* desc, const zpc_params* params, const zpc_batch* host, void* stream);
+
+const char* zpc_status_string(int code);
+int zpc_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ZIPC_H_ */

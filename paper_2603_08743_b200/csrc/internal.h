@@ -1,0 +1,82 @@
+// Library-private declarations for libzipc.so (sm_100a). Not part of the ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include "zipc.h"
+
+namespace zpc {
+
+// Resolved workspace pointers for one call (device addresses).
+struct Ws {
+  float* scores;           // [R][L][h_kv][max_seq_len]
+  int32_t* kept;           // [R][L][h_kv][kept_stride]
+  int32_t* targets;        // [R][n_max-1]
+  int32_t* reserved;       // [R]
+  int32_t* n_prefix;       // [R]
+  float* lse;              // [R][L][h_kv][G*w]
+  unsigned long long* moves;
+  // internal
+  int32_t* req_err;        // [R]
+  int32_t* n_blocks;       // [R]
+  int32_t* fresh_off;      // [R]  exclusive scan of fresh pops
+  int32_t* priv_off;       // [R]  exclusive scan of private frees
+  int32_t* glob;           // [8]  0: total_fresh 1: total_priv 2: top_base 3: n_zeroed
+  int32_t* marks;          // [N_total] shared blocks driven to 0 (ZPC_F_PREFIX)
+  int32_t kept_stride;
+};
+
+// Flattened view of one call: geometry + pointers. Passed by value to kernels.
+struct Call {
+  int32_t L, h_kv, h_q, G, d, b, N_total, M, w, dtype;
+  int32_t n_max, pool_kernel, max_seq_len;
+  uint32_t flags;
+  int32_t R, table_stride, free_capacity, freed_capacity;
+  void* k_cache;
+  void* v_cache;
+  const void* q_cache;
+  const int32_t* q_slots;
+  const int32_t* seq_lens;
+  int32_t* tables;
+  const int32_t* budgets;
+  int32_t* new_lens;
+  int32_t* new_num_blocks;
+  int32_t* ref_counts;
+  int32_t* free_stack;
+  int32_t* free_top;
+  int32_t* freed;
+  int32_t* num_freed;
+  int32_t* status;
+  Ws ws;
+};
+
+// Element offset of row (layer l, physical block blk, slot s, kv head h) in K/V.
+__host__ __device__ inline size_t kv_row(const Call& c, int l, int blk, int s, int h) {
+  return ((((size_t)l * c.N_total + blk) * c.b + s) * c.h_kv + h) * (size_t)c.d;
+}
+// Element offset of the query row (layer l, slot j, window row u, query head hq).
+__host__ __device__ inline size_t q_row(const Call& c, int l, int slot, int u, int hq) {
+  return ((((size_t)l * c.M + slot) * c.w + u) * c.h_q + hq) * (size_t)c.d;
+}
+
+// Kernel launchers (return cudaError_t of the launch).
+cudaError_t launch_plan(const Call& c, cudaStream_t s);
+cudaError_t launch_finalize(const Call& c, cudaStream_t s);
+cudaError_t launch_score_cudacore(const Call& c, cudaStream_t s);
+cudaError_t launch_score_tc(const Call& c, cudaStream_t s, bool* used);
+cudaError_t launch_select(const Call& c, cudaStream_t s);
+cudaError_t launch_compact(const Call& c, cudaStream_t s);
+
+// ---- device helpers ----
+__device__ __forceinline__ float ex2f(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float lg2f(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float bf16_to_f32(uint16_t v) { return __uint_as_float(((uint32_t)v) << 16); }
+
+}  // namespace zpc

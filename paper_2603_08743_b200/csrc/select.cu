@@ -1,0 +1,158 @@
+// a3 + a4: MaxPool1D + window pin + per-head top-l with the
+// index tie rule (R7: score desc, position desc), emitted ascending. One CTA per unit (r, l, h).
+// Selection is an exact 4-pass MSB radix select over order-preserving uint32 keys held in shared
+// memory, followed by a deterministic two-scan emission — no sort, no atomics decide the result.
+#include "internal.h"
+
+namespace zpc {
+namespace {
+
+constexpr int kThreads = 1024;
+constexpr int kWarps = kThreads / 32;
+
+// fp32 -> uint32 with the same order (for finite values and +inf); -0 canonicalised to +0.
+__device__ __forceinline__ uint32_t orderable(float f) {
+  uint32_t u = __float_as_uint(f);
+  if (u == 0x80000000u) u = 0;
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+__device__ __forceinline__ int warp_incl_scan(int x) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  return x;
+}
+
+// exclusive prefix over threads in index order; *total = sum
+__device__ int block_excl(int v, int* sm, int* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int x = warp_incl_scan(v);
+  if (lane == 31) sm[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int s = sm[lane];
+    s = warp_incl_scan(s);
+    sm[lane] = s;
+  }
+  __syncthreads();
+  const int off = (warp ? sm[warp - 1] : 0) + x - v;
+  *total = sm[kWarps - 1];
+  __syncthreads();
+  return off;
+}
+
+__global__ void __launch_bounds__(kThreads) k_select(Call c) {
+  if (*c.status != ZPC_OK) return;
+  extern __shared__ uint32_t keys[];            // [T]
+  __shared__ int hist[256];
+  __shared__ int sm[kWarps];
+  __shared__ uint32_t s_prefix;
+  __shared__ int s_need;
+
+  const int unit = blockIdx.x;
+  const int h = unit % c.h_kv;
+  const int l = (unit / c.h_kv) % c.L;
+  const int r = unit / (c.h_kv * c.L);
+  const int T = c.seq_lens[r];
+  const int ell = min(T, c.budgets[unit]);
+  if (threadIdx.x == 0) c.new_lens[unit] = ell;
+  const float* S = c.ws.scores + (size_t)unit * c.max_seq_len;
+  const int half = c.pool_kernel / 2;
+
+  // load + pool + pin -> keys
+  for (int t = threadIdx.x; t < T; t += kThreads) {
+    float v;
+    if (t >= T - c.w) {
+      v = __int_as_float(0x7f800000);            // +inf: observation window is always kept
+    } else {
+      v = S[t];
+      const int lo = max(0, t - half), hi = min(T - 1, t + half);
+      for (int j = lo; j <= hi; ++j) v = fmaxf(v, S[j]);
+    }
+    keys[t] = orderable(v);
+  }
+  if (threadIdx.x == 0) { s_prefix = 0; s_need = ell; }
+  __syncthreads();
+
+  // MSB radix select of the ell-th largest key
+  uint32_t mask = 0;
+#pragma unroll 1
+  for (int shift = 24; shift >= 0; shift -= 8) {
+    for (int i = threadIdx.x; i < 256; i += kThreads) hist[i] = 0;
+    __syncthreads();
+    const uint32_t prefix = s_prefix;
+    for (int t = threadIdx.x; t < T; t += kThreads) {
+      const uint32_t k = keys[t];
+      if ((k & mask) == prefix) atomicAdd(&hist[(k >> shift) & 255], 1);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      // find digit d: count(>d) < need <= count(>=d), scanning from 255 down (warp 0)
+      const int lane = threadIdx.x;
+      // each lane owns 8 consecutive digits, lane 0 the highest
+      int cnt[8];
+      int sum = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) { cnt[i] = hist[255 - (lane * 8 + i)]; sum += cnt[i]; }
+      int incl = warp_incl_scan(sum);
+      const int excl = incl - sum;                 // count of keys with digit above this lane's range
+      const int need = s_need;
+      int found = -1, above = 0;
+      int run = excl;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if (found < 0 && run < need && run + cnt[i] >= need) { found = 255 - (lane * 8 + i); above = run; }
+        run += cnt[i];
+      }
+      const unsigned ball = __ballot_sync(0xffffffffu, found >= 0);
+      const int src = __ffs(ball) - 1;
+      const int d = __shfl_sync(0xffffffffu, found, src);
+      const int ab = __shfl_sync(0xffffffffu, above, src);
+      if (lane == 0) { s_prefix = prefix | ((uint32_t)d << shift); s_need = need - ab; }
+    }
+    mask |= 0xffu << shift;
+    __syncthreads();
+  }
+  const uint32_t kstar = s_prefix;
+  const int need_eq = s_need;   // how many keys == kstar to keep: the latest positions
+
+  // emission: contiguous chunk per thread
+  const int chunk = (T + kThreads - 1) / kThreads;
+  const int t0 = min(T, threadIdx.x * chunk), t1 = min(T, t0 + chunk);
+  int eq = 0;
+  for (int t = t0; t < t1; ++t) eq += (keys[t] == kstar);
+  int eq_tot;
+  const int eq_before = block_excl(eq, sm, &eq_tot);
+  int eq_after = eq_tot - eq_before - eq;      // equal keys at later positions than this chunk
+  int kept_here = 0;
+  for (int t = t1 - 1; t >= t0; --t) {
+    const uint32_t k = keys[t];
+    bool keep = k > kstar;
+    if (k == kstar) { keep = eq_after < need_eq; ++eq_after; }
+    kept_here += keep;
+    keys[t] = keep ? 1u : 0u;                  // reuse as flag (own chunk only)
+  }
+  int kept_tot;
+  const int out0 = block_excl(kept_here, sm, &kept_tot);
+  int32_t* out = c.ws.kept + (size_t)unit * c.ws.kept_stride;
+  int o = out0;
+  for (int t = t0; t < t1; ++t)
+    if (keys[t]) out[o++] = t;
+}
+
+}  // namespace
+
+cudaError_t launch_select(const Call& c, cudaStream_t s) {
+  const int units = c.R * c.L * c.h_kv;
+  if (units == 0) return cudaSuccess;
+  const size_t smem = sizeof(uint32_t) * (size_t)c.max_seq_len;
+  cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_select<<<units, kThreads, smem, s>>>(c);
+  return cudaGetLastError();
+}
+
+}  // namespace zpc

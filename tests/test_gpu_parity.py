@@ -1,0 +1,167 @@
+"""GPU parity: the CUDA path through the C ABI vs the fp64 oracle on the same seeded inputs.
+
+Rules: scores within 1e-3 relative; kept sets exact outside
+the 1e-3 band around the oracle's ell-th score; GPU S through the oracle's select reproduces
+the GPU kept list bit for bit; whole K/V pools, tables, freed list, free stack and ref counts
+bit-exact against oracle compaction driven by the GPU's kept lists.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from paper_2603_08743_b200 import zipc
+from paper_2603_08743_b200.batch import batch_of, desc_params
+from zpc_inputs import CONFIGS, make_host_workload, scaled
+from zpc_inputs.device import from_host, generate, to_host
+
+from helpers import full_check, gpu_results, run_gpu, snapshot_inputs
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(cfg, seed=0, flags=0, pool=None, stages=False, strict=True, max_seq_len=None):
+    hw = make_host_workload(cfg, seed)
+    w = from_host(hw, max_seq_len=max_seq_len)
+    inp = snapshot_inputs(w)
+    desc, params = run_gpu(w, flags=flags, pool=pool, stages=stages)
+    res = gpu_results(w, desc, params)
+    full_check(w, inp, res, pool=pool, strict_select=strict)
+    return w, res
+
+
+@pytest.mark.parametrize("pool", [1, 3])
+def test_fig1_toy(cuda_ok, pool):
+    """BASELINE configs[0]: the Fig. 1 toy (fp32, CUDA-core scoring)."""
+    cfg = scaled(CONFIGS["toy"], pool_kernel=pool)
+    w, res = _run(cfg, seed=1, pool=pool)
+    lay = w.layout
+    A, B = lay.tables[0], lay.tables[1]
+    assert res["freed"].tolist() == [A[4], B[4], B[5], B[6]]
+
+
+def test_toy_stagewise_equals_fused(cuda_ok):
+    cfg = CONFIGS["toy"]
+    _run(cfg, seed=2, stages=True)
+
+
+SMALL7B = scaled(CONFIGS["qwen7b"], L=2, h_kv=2, h_q=14, n_max=9, seq_lens=[300, 257, 416, 129 + 128],
+                 budget=128, free_slack=5)
+
+
+@pytest.mark.parametrize("flags", [0, zipc.ZPC_F_SCORE_CUDACORE])
+def test_qwen7b_shape_small(cuda_ok, flags):
+    """7B head shape (G=7, w=32, d=128, b=16, bf16), ragged T spanning several 128-token tiles."""
+    _run(SMALL7B, seed=3, flags=flags)
+
+
+def test_llama8b_shape_mixed_budgets(cuda_ok):
+    cfg = scaled(CONFIGS["llama8b"], L=2, h_kv=2, h_q=8, n_max=9, seq_lens=[513, 700, 1030], budget=(32, 128),
+                 wave=0)
+    _run(cfg, seed=4)
+
+
+def test_qwen32b_shape_d64_variant(cuda_ok):
+    cfg = scaled(CONFIGS["qwen32b"], L=2, h_kv=2, h_q=10, d=64, n_max=6, seq_lens=[200, 333], budget=80, wave=0)
+    _run(cfg, seed=5)
+
+
+def test_prefix_small(cuda_ok):
+    """§4.5 shared prefix with the harness holding a reference: fresh targets + own reuse."""
+    for npref_tok, seq in [(64, 300), (160, 400), (256, 300)]:
+        cfg = scaled(CONFIGS["prefix"], L=2, h_kv=2, h_q=14, n_max=9, seq_lens=[seq] * 3, prefix_tokens=npref_tok,
+                     budget=128, wave=0, free_slack=4)
+        _run(cfg, seed=6)
+
+
+def test_edge_min_trigger_and_w_gt_b(cuda_ok):
+    """N == N_max exactly, partial last block, w > b, budget == w."""
+    cfg = scaled(CONFIGS["qwen7b"], L=1, h_kv=1, h_q=7, n_max=3, seq_lens=[33, 48, 40], budget=32, free_slack=2)
+    _run(cfg, seed=7)
+
+
+def test_generator_device_equals_host(cuda_ok):
+    cfg = scaled(CONFIGS["prefix"], L=2, h_kv=2, h_q=14, n_max=9, seq_lens=[300] * 2, prefix_tokens=64, wave=0)
+    hw = make_host_workload(cfg, 11)
+    dw = generate(cfg, 11, np.arange(2))
+    np.testing.assert_array_equal(to_host(dw.k, True), hw.k_cache)
+    np.testing.assert_array_equal(to_host(dw.v, True), hw.v_cache)
+    np.testing.assert_array_equal(to_host(dw.q, True), hw.q_cache)
+
+
+@pytest.mark.parametrize("case", ["not_triggered", "bad_budget", "no_free", "bad_slot", "bad_table"])
+def test_device_errors_mutate_nothing(cuda_ok, case):
+    cfg = scaled(CONFIGS["prefix"], L=1, h_kv=2, h_q=14, n_max=9, seq_lens=[300, 300], prefix_tokens=64,
+                 budget=128, wave=0, free_slack=4)
+    hw = make_host_workload(cfg, 8)
+    expect = {"not_triggered": zipc.ZPC_ERR_NOT_TRIGGERED, "bad_budget": zipc.ZPC_ERR_BAD_BUDGET,
+              "no_free": zipc.ZPC_ERR_NO_FREE_BLOCKS, "bad_slot": zipc.ZPC_ERR_BAD_SLOT,
+              "bad_table": zipc.ZPC_ERR_BAD_TABLE}[case]
+    lay = hw.layout
+    if case == "not_triggered":
+        lay.seq_lens[1] = 16 * 8
+    elif case == "bad_budget":
+        hw.budgets[1, 0, 1] = 8 * 16 + 1
+    elif case == "no_free":
+        lay.free_top = 3
+    elif case == "bad_slot":
+        lay.q_slots[0] = lay.M
+    elif case == "bad_table":
+        lay.tables[1, 10] = lay.N_total
+    w = from_host(hw)
+    before = snapshot_inputs(w)
+    desc, params = run_gpu(w)
+    assert int(w.status.item()) == expect
+    np.testing.assert_array_equal(to_host(w.k, True), before["k"])
+    np.testing.assert_array_equal(to_host(w.tables), before["tables"])
+    np.testing.assert_array_equal(to_host(w.free_stack), before["stack"])
+    assert int(w.free_top.item()) == before["top"]
+    np.testing.assert_array_equal(to_host(w.ref_counts), before["refs"])
+    # oracle agrees on the code
+    ref = O.plan(O.Geometry(cfg.L, cfg.h_kv, cfg.h_q, cfg.d, cfg.b, lay.N_total, lay.M, cfg.w, cfg.dtype),
+                 O.Params(cfg.n_max, flags=O.F_PREFIX, max_seq_len=w.max_seq_len), before["seq"],
+                 before["tables"], before["budgets"], before["refs"], before["stack"], before["top"],
+                 before["slots"])
+    assert ref.status == expect
+
+
+def test_host_variant_equals_device(cuda_ok):
+    """zpc_compress_host (host bookkeeping, copies inside the call) == zpc_compress."""
+    hw = make_host_workload(SMALL7B, 9)
+    w1 = from_host(hw)
+    run_gpu(w1)
+    w2 = from_host(hw)
+    desc, params = desc_params(w2)
+    R = int(w2.seq_lens.numel())
+    pin = lambda t: t.cpu().pin_memory()  # noqa: E731
+    host = {k: pin(getattr(w2, k)) for k in ("q_slots", "seq_lens", "tables", "budgets", "new_lens",
+                                            "new_num_blocks", "free_stack", "free_top", "freed", "num_freed",
+                                            "status")}
+    need = zipc.zpc_workspace_bytes_host(desc, params, R, host["tables"].shape[1], host["free_stack"].numel(),
+                                         host["freed"].numel())
+    ws = torch.empty(need, dtype=torch.uint8, device="cuda")
+    b = zipc.make_batch(k_cache=w2.k, v_cache=w2.v, q_cache=w2.q, q_slots=host["q_slots"],
+                        seq_lens=host["seq_lens"], block_tables=host["tables"], budgets=host["budgets"],
+                        new_lens=host["new_lens"], new_num_blocks=host["new_num_blocks"], ref_counts=None,
+                        free_stack=host["free_stack"], free_top=host["free_top"], freed_blocks=host["freed"],
+                        num_freed=host["num_freed"], workspace=ws, status=host["status"])
+    zipc.zpc_compress_host(desc, params, b)
+    torch.cuda.synchronize()
+    assert int(host["status"][0]) == 0
+    assert torch.equal(w1.k.cpu(), w2.k.cpu()) and torch.equal(w1.v.cpu(), w2.v.cpu())
+    assert torch.equal(w1.tables.cpu(), host["tables"])
+    n = int(host["num_freed"][0])
+    assert n == int(w1.num_freed.item())
+    assert torch.equal(w1.freed.cpu()[:n], host["freed"][:n])
+    assert torch.equal(w1.new_lens.cpu(), host["new_lens"])
+
+
+def test_deterministic(cuda_ok):
+    hw = make_host_workload(SMALL7B, 10)
+    outs = []
+    for _ in range(2):
+        w = from_host(hw)
+        desc, params = run_gpu(w)
+        outs.append(gpu_results(w, desc, params))
+    for key in ("S", "kept", "k", "v", "tables", "freed", "stack"):
+        np.testing.assert_array_equal(outs[0][key], outs[1][key])
