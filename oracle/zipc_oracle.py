@@ -155,11 +155,17 @@ def plan(geo: Geometry, prm: Params, seq_lens, tables, budgets, ref_counts=None,
     if demand > top:
         return Plan(status=ERR_NO_FREE_BLOCKS)
     if freed_capacity is not None or free_capacity is not None:
+        # R18: capacity is checked against exactly the blocks the call will free — private
+        # non-target blocks plus shared blocks whose every reference is held by this batch.
         priv = sum(max(0, int(nb[r]) - 1 - max(int(npf[r]), nm1)) for r in range(R))
-        shared_entries = int(sum(npf))
-        if freed_capacity is not None and priv + shared_entries > freed_capacity:
+        occ = {}
+        for r in range(R):
+            for j in range(int(npf[r])):
+                occ[int(tables[r, j])] = occ.get(int(tables[r, j]), 0) + 1
+        zeroed = sum(1 for bid, n in occ.items() if n == ref_counts[bid])
+        if freed_capacity is not None and priv + zeroed > freed_capacity:
             return Plan(status=ERR_CAPACITY)
-        if free_capacity is not None and top - demand + priv + shared_entries > free_capacity:
+        if free_capacity is not None and top - demand + priv + zeroed > free_capacity:
             return Plan(status=ERR_CAPACITY)
     for r in range(R):
         N, n_prefix = int(nb[r]), int(npf[r])

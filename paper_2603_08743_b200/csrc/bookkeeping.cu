@@ -100,6 +100,9 @@ __global__ void __launch_bounds__(256) k_plan_req(Call c) {
     if (__syncthreads_or(bad)) err = ZPC_ERR_BAD_BUDGET;
   }
   (void)s_err;
+  // occurrences of each shared block in this batch (exact capacity check, R18)
+  if (err == ZPC_OK)
+    for (int j = threadIdx.x; j < np; j += blockDim.x) atomicAdd(&c.ws.marks[table[j]], 1);
   if (threadIdx.x == 0) {
     c.ws.req_err[r] = err;
     c.ws.n_blocks[r] = N;
@@ -122,34 +125,39 @@ __global__ void __launch_bounds__(kScanThreads) k_plan_scan(Call c) {
     return;
   }
   // exclusive scans over requests (chunks of kScanThreads)
-  int fresh_base = 0, priv_base = 0, shared_base = 0;
+  int fresh_base = 0, priv_base = 0, zeroed = 0;
+  if (c.ref_counts && (c.flags & ZPC_F_PREFIX)) {
+    int z = 0;
+    for (int i = threadIdx.x; i < c.N_total; i += blockDim.x) {
+      const int occ = c.ws.marks[i];
+      z += (occ > 0 && occ == c.ref_counts[i]);
+    }
+    block_exclusive_scan<kScanThreads>(z, &zeroed, sm);
+  }
   for (int r0 = 0; r0 < c.R; r0 += kScanThreads) {
     const int r = r0 + threadIdx.x;
-    int nf = 0, npv = 0, nsh = 0;
+    int nf = 0, npv = 0;
     if (r < c.R) {
       const int N = c.ws.n_blocks[r], np = c.ws.n_prefix[r];
       const int res_idx = max(np, nm1);
       nf = min(np, nm1) + (res_idx >= N ? 1 : 0);
       npv = max(0, N - 1 - res_idx);
-      nsh = np;
     }
-    int tf, tp, ts;
+    int tf, tp;
     int of = block_exclusive_scan<kScanThreads>(nf, &tf, sm);
     int op = block_exclusive_scan<kScanThreads>(npv, &tp, sm);
-    block_exclusive_scan<kScanThreads>(nsh, &ts, sm);
     if (r < c.R) {
       c.ws.fresh_off[r] = fresh_base + of;
       c.ws.priv_off[r] = priv_base + op;
     }
     fresh_base += tf;
     priv_base += tp;
-    shared_base += ts;
   }
   const int top = *c.free_top;
   int st = ZPC_OK;
   if (fresh_base > top) st = ZPC_ERR_NO_FREE_BLOCKS;
-  else if ((long long)priv_base + shared_base > c.freed_capacity) st = ZPC_ERR_CAPACITY;
-  else if ((long long)top - fresh_base + priv_base + shared_base > c.free_capacity) st = ZPC_ERR_CAPACITY;
+  else if ((long long)priv_base + zeroed > c.freed_capacity) st = ZPC_ERR_CAPACITY;
+  else if ((long long)top - fresh_base + priv_base + zeroed > c.free_capacity) st = ZPC_ERR_CAPACITY;
   if (st != ZPC_OK) {
     if (threadIdx.x == 0) *c.status = st;
     return;
@@ -194,7 +202,7 @@ __global__ void __launch_bounds__(256) k_finalize_req(Call c) {
   if (c.ref_counts && (c.flags & ZPC_F_PREFIX)) {
     for (int j = threadIdx.x; j < np; j += blockDim.x) {
       const int id = table[j];
-      if (atomicSub(&c.ref_counts[id], 1) == 1) c.ws.marks[id] = 1;
+      atomicSub(&c.ref_counts[id], 1);
     }
   }
   __syncthreads();
@@ -220,7 +228,7 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize_tail(Call c) {
   if (c.ref_counts && (c.flags & ZPC_F_PREFIX)) {
     for (int i0 = 0; i0 < c.N_total; i0 += kScanThreads) {
       const int i = i0 + threadIdx.x;
-      const int m = (i < c.N_total) ? c.ws.marks[i] : 0;
+      const int m = (i < c.N_total) ? (c.ws.marks[i] > 0 && c.ref_counts[i] == 0) : 0;
       int tot;
       const int off = block_exclusive_scan<kScanThreads>(m, &tot, sm);
       if (m) c.freed[base + off] = i;
@@ -242,9 +250,9 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize_tail(Call c) {
 }  // namespace
 
 cudaError_t launch_plan(const Call& c, cudaStream_t s) {
-  if (c.R > 0) k_plan_req<<<c.R, 256, 0, s>>>(c);
   if (c.ref_counts && (c.flags & ZPC_F_PREFIX))
     cudaMemsetAsync(c.ws.marks, 0, sizeof(int32_t) * (size_t)c.N_total, s);
+  if (c.R > 0) k_plan_req<<<c.R, 256, 0, s>>>(c);
   k_plan_scan<<<1, kScanThreads, 0, s>>>(c);
   return cudaGetLastError();
 }
