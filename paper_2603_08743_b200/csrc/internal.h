@@ -30,6 +30,7 @@ struct Call {
   int32_t L, h_kv, h_q, G, d, b, N_total, M, w, dtype;
   int32_t n_max, pool_kernel, max_seq_len;
   uint32_t flags;
+  uint32_t debug;      // tuning/bisection switches (ZPC_SCORE_DEBUG), 0 in production
   int32_t R, table_stride, free_capacity, freed_capacity;
   void* k_cache;
   void* v_cache;

@@ -17,9 +17,11 @@
 //  * A unit's tokens are split across a C-CTA cluster; partial (max, sum) per column are combined
 //    through DSMEM, so pass 2 re-reads a CTA-sized slice of K (L2-resident) instead of the unit.
 //  * Warp roles: warp 0 TMA producer, warp 1 TMEM allocator + MMA issuer (one thread), warps 2..9
-//    epilogue (two per TMEM lane quarter). K ring of kStages smem stages, two TMEM accumulators.
+//    epilogue (two per TMEM lane quarter). K ring of K::ST smem stages, two TMEM accumulators,
+//    persistent CTAs looping over units, Q double-buffered by TMA.
 #include <cuda.h>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "internal.h"
@@ -28,12 +30,16 @@ namespace zpc {
 namespace {
 
 constexpr int kTile = 128;       // tokens per tile (UMMA M in pass 2, N in pass 1)
-constexpr int kStages = 4;       // K smem ring depth
-constexpr int kThreads = 320;    // 10 warps
+constexpr int kThreads = 512;    // 16 warps: Q-TMA, MMA, table walker, spare, 4 K loaders, 8 epilogue
+constexpr int kLoadWarps = 4;
+constexpr int kEpiWarp0 = 8;     // first epilogue warp (warps 8..15: lane quarter = warp % 4)
+constexpr int kIdSlots = 8;      // block-id ring (steps) filled by the walker, 4 steps per group
+constexpr int kIdGroup = 4;
+constexpr int kMaxIds = 32;      // block ids per 128-token tile (b >= 5)
 constexpr int kEpiWarps = 8;
+constexpr uint32_t kL1Reserve = 0;   // L1 left unallocated (cp.async does not need it: measured)
 constexpr uint32_t kTmemCols = 512;
 constexpr float kLog2e = 1.4426950408889634f;
-constexpr int kPolyEvery = 0;   // every k-th pass-1 exp on the FMA pipe (0 = MUFU only)
 
 // ------------------------------------------------------------------ PTX wrappers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -52,13 +58,14 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   uint32_t done = 0;
   long long spins = 0;
   while (true) {
+    // suspend-time hint: the thread sleeps until the phase completes (or ~1 ms), no busy polling
     asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
         : "=r"(done)
-        : "r"(bar), "r"(parity)
+        : "r"(bar), "r"(parity), "r"(1000000)
         : "memory");
     if (done) return;
-    if (++spins > (1LL << 26)) __trap();   // a pipeline bug must fail loudly, never hang the GPU
+    if (++spins > (1LL << 22)) __trap();   // a pipeline bug must fail loudly, never hang the GPU
   }
 }
 __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2,
@@ -69,6 +76,24 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map
       ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar), "l"(policy)
       : "memory");
 }
+__device__ __forceinline__ int lds_s32(uint32_t addr) {
+  int v;
+  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, int /*unused*/) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+// the mbarrier counts this thread's arrival once all its prior cp.async have landed
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void cp_async_arrive_noinc(uint32_t bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
+}
+
 __device__ __forceinline__ uint64_t policy_evict_last() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
@@ -145,295 +170,545 @@ __device__ __forceinline__ float ld_dsmem_f32(const float* local, uint32_t rank)
   return v;
 }
 
+// ------------------------------------------------------------------ packed fp32x2 + misc helpers
+__device__ __forceinline__ uint64_t pk2(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void upk2(uint64_t r, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+__device__ __forceinline__ uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t add2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ float max3f(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+// packed 2^x, x <= 0, on the FMA pipe (see ex2_poly)
+__device__ __forceinline__ uint64_t ex2_poly2(uint64_t x2) {
+  float x0, x1;
+  upk2(x2, x0, x1);
+  x2 = pk2(fmaxf(x0, -125.f), fmaxf(x1, -125.f));
+  const uint64_t t2 = add2(x2, pk2(12582912.f, 12582912.f));
+  const uint64_t n2 = add2(t2, pk2(-12582912.f, -12582912.f));
+  const uint64_t f2 = fma2(n2, pk2(-1.f, -1.f), x2);
+  uint64_t p = fma2(pk2(1.3534167e-4f, 1.3534167e-4f), f2, pk2(1.3395720e-3f, 1.3395720e-3f));
+  p = fma2(p, f2, pk2(9.6180239e-3f, 9.6180239e-3f));
+  p = fma2(p, f2, pk2(5.5504109e-2f, 5.5504109e-2f));
+  p = fma2(p, f2, pk2(2.4022652e-1f, 2.4022652e-1f));
+  p = fma2(p, f2, pk2(6.9314718e-1f, 6.9314718e-1f));
+  p = fma2(p, f2, pk2(1.0f, 1.0f));
+  float p0, p1, t0, t1;
+  upk2(p, p0, p1);
+  upk2(t2, t0, t1);
+  // (bits(t) - bits(1.5*2^23)) << 23 == bits(t) << 23 (mod 2^32): the magic's low 9 bits are 0
+  return pk2(__int_as_float(__float_as_int(p0) + (__float_as_int(t0) << 23)),
+             __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23)));
+}
+__device__ __forceinline__ void mbar_remote_arrive(uint32_t local_bar, uint32_t rank) {
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(local_bar), "r"(rank));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(ra) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  long long spins = 0;
+  while (true) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2, %3;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(parity), "r"(1000000)
+        : "memory");
+    if (done) return;
+    if (++spins > (1LL << 26)) __trap();
+  }
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 // ------------------------------------------------------------------ kernel
 template <int G, int W, int D, int C>
 struct Cfg {
   static constexpr int GW = G * W;
-  static constexpr int M1H = (GW + 127) / 128;        // pass-1 M halves (A = Q rows)
-  static constexpr int NQ = M1H * 128;                 // padded Q rows in smem
+  static constexpr int M1H = (GW + 127) / 128;        // pass-1 M halves (A = Q rows; rows >= GW are
+                                                      // whatever follows in smem: their D rows are unused)
   static constexpr int SLABS = D / 64;                 // 64-element (128 B) K-chunks
   static constexpr int KSTEPS = D / 16;                // UMMA K = 16 per instruction
   static constexpr int HC = (W / 2) * G;               // pass-2 columns per epilogue half
-  static constexpr uint32_t Q_BYTES = NQ * D * 2;
-  static constexpr uint32_t SLAB_Q = NQ * 128;         // bytes per Q slab
+  static constexpr int UB = 4;                         // window rows per pass-2 batch
+  static constexpr int LDMAX = (UB * G + 15) / 16 + 1;  // 16-column TMEM loads per batch (upper bound)
+  static constexpr uint32_t SLAB_Q = GW * 128;         // bytes per Q slab (GW rows of 128 B)
+  static constexpr uint32_t Q_BYTES = SLAB_Q * SLABS;
   static constexpr uint32_t SLAB_K = kTile * 128;      // bytes per K slab
   static constexpr uint32_t STAGE_BYTES = kTile * D * 2;
+  static constexpr uint32_t MISC = (2 * 256 * 2 + 256 + 2 * kTile) * 4 + kIdSlots * kMaxIds * 4 + 56 * 8 + 16;
+  // Shared memory and L1 are one 228 KB array on sm_100: the cp.async gather stages its in-flight
+  // lines through L1, so the kernel leaves kL1Reserve bytes of it unallocated (DESIGN.md §Score
+  // kernel, "L1 is the gather's in-flight buffer"). Q is therefore single-buffered.
+  static constexpr int STAGES_FIT = (int)((227 * 1024 - kL1Reserve - 1024 - MISC - Q_BYTES) / STAGE_BYTES);
+  static constexpr int ST = STAGES_FIT > 6 ? 6 : STAGES_FIT;   // K ring depth
+  static constexpr uint32_t OFF_Q0 = 0;
   static constexpr uint32_t OFF_K = Q_BYTES;
-  static constexpr uint32_t OFF_F = OFF_K + kStages * STAGE_BYTES;   // floats: negL, pm, ps, comb
-  static constexpr uint32_t OFF_BAR = OFF_F + (256 * 3 + 256) * 4;
-  static constexpr uint32_t SMEM = OFF_BAR + 16 * 8 + 16 + 1024;      // + alignment slack
+  static constexpr uint32_t OFF_F = OFF_K + ST * STAGE_BYTES;        // floats
+  static constexpr uint32_t OFF_IDS = OFF_F + (2 * 256 * 2 + 256 + 2 * kTile) * 4;
+  static constexpr uint32_t OFF_BAR = OFF_IDS + kIdSlots * kMaxIds * 4;
+  static constexpr uint32_t SMEM = OFF_BAR + 56 * 8 + 16 + 1024;     // + alignment slack
   static_assert(GW % 16 == 0 && GW <= 256, "pass-2 UMMA N must be a multiple of 16, <= 256");
-  static_assert(HC % 16 == 0, "epilogue loads 16 columns at a time");
-  static_assert(W % 2 == 0, "window split across two epilogue halves");
+  static_assert(W == 32, "epilogue batching assumes w = 32");
+  static_assert(ST >= 2, "K ring needs >= 2 stages");
+  static_assert(Q_BYTES % 1024 == 0, "Q slabs must stay 1024-B aligned for SW128");
 };
 
+// 2^x on MUFU for most pairs, on the FMA pipe for pairs j % 4 == 3 (25%): balances the two pipes.
+template <int J>
+__device__ __forceinline__ uint64_t ex2_pair(uint64_t a2) {
+  if constexpr ((J & 3) == 3) {
+    return ex2_poly2(a2);
+  } else {
+    float a0, a1;
+    upk2(a2, a0, a1);
+    return pk2(ex2f(a0), ex2f(a1));
+  }
+}
+
+// sum_j 2^(v[j]*scale - m) over a 64-value batch, packed
+template <int J>
+__device__ __forceinline__ void sum_exp_rec(const float* v, uint64_t S2, uint64_t NM2, uint64_t* acc) {
+  if constexpr (J < 32) {
+    const uint64_t arg = fma2(pk2(v[2 * J], v[2 * J + 1]), S2, NM2);
+    acc[J & 3] = add2(acc[J & 3], ex2_pair<J>(arg));
+    sum_exp_rec<J + 1>(v, S2, NM2, acc);
+  }
+}
+__device__ __forceinline__ float sum_exp64(const float* v, float scale, float m) {
+  uint64_t acc[4] = {0, 0, 0, 0};
+  sum_exp_rec<0>(v, pk2(scale, scale), pk2(-m, -m), acc);
+  const uint64_t s2 = add2(add2(acc[0], acc[1]), add2(acc[2], acc[3]));
+  float a, b;
+  upk2(s2, a, b);
+  return a + b;
+}
+
 template <int G, int W, int D, int C>
-__global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_constant__ CUtensorMap tmap_k) {
+__global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_constant__ CUtensorMap tmap_q) {
   using K = Cfg<G, W, D, C>;
   if (*c.status != ZPC_OK) return;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* Qs = smem;
   uint8_t* Ks = smem + K::OFF_K;
-  float* negL = reinterpret_cast<float*>(smem + K::OFF_F);
-  float* pm = negL + 256;
-  float* ps = pm + 256;
-  float* comb = ps + 256;                               // [2][128]
+  float* pmv = reinterpret_cast<float*>(smem + K::OFF_F);   // [2][256] partial max (by unit parity)
+  float* psv = pmv + 512;                                     // [2][256] partial sums
+  float* negL = psv + 512;                                    // [256]
+  float* comb = negL + 256;                                   // [2][128]
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + K::OFF_BAR);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
-  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + kStages);
-  const uint32_t accf0 = smem_u32(bars + 2 * kStages), acce0 = smem_u32(bars + 2 * kStages + 2);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 54);
+  int* ids = reinterpret_cast<int*>(smem + K::OFF_IDS);                  // [kIdSlots][kMaxIds]
+  const uint32_t idf0 = smem_u32(bars + 24), ide0 = smem_u32(bars + 32);  // ids full / empty
+  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + 40);
+  const uint32_t accf0 = smem_u32(bars + 8), acce0 = smem_u32(bars + 10);
+  const uint32_t qfull0 = smem_u32(bars + 12), qempty0 = smem_u32(bars + 14);
+  const uint32_t xchg0 = smem_u32(bars + 16);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int unit = blockIdx.x / C;
   const int rank = C > 1 ? (int)(blockIdx.x % C) : 0;
-  const int h = unit % c.h_kv;
-  const int l = (unit / c.h_kv) % c.L;
-  const int r = unit / (c.h_kv * c.L);
-  const int T = c.seq_lens[r];
-  const int slot = c.q_slots[r];
-  const int ntot = (T + kTile - 1) / kTile;
-  const int tb = (int)((long long)ntot * rank / C), te = (int)((long long)ntot * (rank + 1) / C);
-  const int nt = te - tb;
-  const int* table = c.tables + (size_t)r * c.table_stride;
-  const int Nblk = (T + c.b - 1) / c.b;
+  const int cluster_id = blockIdx.x / C;
+  const int nclusters = gridDim.x / C;
+  const int units = c.R * c.L * c.h_kv;
 
-  // ---- setup: barriers, TMEM, Q tile (swizzled by hand; zero padding rows)
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) { mbar_init(full0 + 8 * s, 1); mbar_init(empty0 + 8 * s, 1); }
-    for (int a = 0; a < 2; ++a) { mbar_init(accf0 + 8 * a, 1); mbar_init(acce0 + 8 * a, kEpiWarps); }
+    for (int s = 0; s < K::ST; ++s) { mbar_init(full0 + 8 * s, kLoadWarps * 32); mbar_init(empty0 + 8 * s, 1); }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(accf0 + 8 * a, 1);
+      mbar_init(acce0 + 8 * a, kEpiWarps);
+      mbar_init(qfull0 + 8 * a, 1);
+      mbar_init(qempty0 + 8 * a, 1);
+      mbar_init(xchg0 + 8 * a, C);
+    }
+    for (int k = 0; k < kIdSlots; ++k) { mbar_init(idf0 + 8 * k, 1); mbar_init(ide0 + 8 * k, kLoadWarps); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 0 && lane == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_k)));
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_q)));
+  }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "r"(kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  {
-    const uint16_t* Q = reinterpret_cast<const uint16_t*>(c.q_cache);
-    constexpr int CH = D / 8;                          // 16-byte chunks per row
-    for (int e = threadIdx.x; e < K::NQ * CH; e += kThreads) {
-      const int row = e / CH, j = e % CH;
-      int4 v = make_int4(0, 0, 0, 0);
-      if (row < K::GW) {
-        const int u = row / G, g = row % G;
-        v = *reinterpret_cast<const int4*>(Q + q_row(c, l, slot, u, h * G + g) + j * 8);
-      }
-      const int slab = j >> 3, jj = j & 7;
-      *reinterpret_cast<int4*>(Qs + slab * K::SLAB_Q + row * 128 + ((jj ^ (row & 7)) << 4)) = v;
-    }
-  }
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   tc_fence_before();
   __syncthreads();
+  if (C > 1) cluster_sync_all();        // peers' barriers are initialised before any remote arrive
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const float scale = kLog2e * rsqrtf((float)D);
 
+  // per-unit geometry, identical in every role
+  struct UnitInfo { int r, l, h, T, slot, tb, nt; };
+  auto unit_info = [&](int unit) {
+    UnitInfo u;
+    u.h = unit % c.h_kv;
+    u.l = (unit / c.h_kv) % c.L;
+    u.r = unit / (c.h_kv * c.L);
+    u.T = c.seq_lens[u.r];
+    u.slot = c.q_slots[u.r];
+    const int ntot = (u.T + kTile - 1) / kTile;
+    u.tb = (int)((long long)ntot * rank / C);
+    u.nt = (int)((long long)ntot * (rank + 1) / C) - u.tb;
+    return u;
+  };
+  // step i of a unit -> tile index: pass 1 ascending, pass 2 DESCENDING (the most recently
+  // streamed tiles are the ones most likely still in L2)
+  auto tile_of = [](const UnitInfo& u, int i) { return i < u.nt ? u.tb + i : u.tb + (2 * u.nt - 1 - i); };
+
   if (warp == 0) {
-    // ================= TMA producer
-    if (C > 1) cluster_arrive_relaxed();
+    // ================= Q producer: one TMA box per 64-element slab per unit (double buffer)
     if (lane == 0) {
-      const uint64_t keep = policy_evict_last(), drop = policy_evict_first();
-      const int rows_box = c.b >= kTile ? kTile : c.b;
-      const int boxes = c.b >= kTile ? 1 : kTile / c.b;
-      for (int i = 0; i < 2 * nt; ++i) {
-        const int s = i % kStages;
-        mbar_wait(empty0 + 8 * s, ((i / kStages) & 1) ^ 1);
-        const int t0 = (tb + i % nt) * kTile;
-        const int j0 = t0 / c.b;
-        int nbox = 1;
-        if (boxes > 1) nbox = min(boxes, Nblk - j0);
-        mbar_expect_tx(full0 + 8 * s, (uint32_t)(nbox * rows_box * 128 * K::SLABS));
-        const uint32_t dst = smem_u32(Ks + s * K::STAGE_BYTES);
-        for (int bx = 0; bx < nbox; ++bx) {
-          const int blk = table[j0 + bx];
-          const int row = (int)(((long long)l * c.N_total + blk) * c.b + (boxes > 1 ? 0 : t0 % c.b));
-          for (int sl = 0; sl < K::SLABS; ++sl)
-            tma_load_3d(dst + sl * K::SLAB_K + bx * rows_box * 128, &tmap_k, sl * 64, h, row, full0 + 8 * s,
-                        i < nt ? keep : drop);
-        }
+      const uint64_t drop = policy_evict_first();
+      for (int it = 0, unit = cluster_id; unit < units; ++it, unit += nclusters) {
+        const UnitInfo u = unit_info(unit);
+        const int qb = 0;                    // single Q buffer (see kL1Reserve)
+        mbar_wait(qempty0, (it & 1) ^ 1);
+        if (c.debug & 32u) { mbar_arrive(qfull0); continue; }   // bisection: no Q load
+        mbar_expect_tx(qfull0, K::Q_BYTES);
+        const uint32_t qdst = smem_u32(smem + K::OFF_Q0);
+        const int qrow = (u.l * c.M + u.slot) * W;
+        for (int sl = 0; sl < K::SLABS; ++sl)
+          tma_load_3d(qdst + sl * K::SLAB_Q, &tmap_q, sl * 64, u.h * G, qrow, qfull0 + 8 * qb, drop);
       }
     }
     __syncwarp();
-    if (C > 1) cluster_wait();
+  } else if (warp == 2) {
+    // ================= table walker: block ids of every K tile, kIdGroup steps at a time, into a
+    // shared ring, so the gathering threads never wait on a table load (DESIGN.md §Score kernel)
+    int w_unit = cluster_id, w_i = 0, g = 0;
+    UnitInfo w_u = w_unit < units ? unit_info(w_unit) : UnitInfo{};
+    while (true) {
+      int gs = 0;
+      int t0s[kIdGroup], js[kIdGroup], nbs[kIdGroup];
+      const int* tbl[kIdGroup];
+#pragma unroll
+      for (int k = 0; k < kIdGroup; ++k) {
+        while (w_unit < units && w_i >= 2 * w_u.nt) {
+          w_unit += nclusters;
+          w_i = 0;
+          if (w_unit < units) w_u = unit_info(w_unit);
+        }
+        nbs[k] = 0;
+        if (w_unit < units) {
+          t0s[k] = tile_of(w_u, w_i) * kTile;
+          js[k] = t0s[k] / c.b;
+          nbs[k] = (min(t0s[k] + kTile, w_u.T) - 1) / c.b - js[k] + 1;
+          tbl[k] = c.tables + (size_t)w_u.r * c.table_stride;
+          ++w_i;
+          ++gs;
+        }
+      }
+      if (gs == 0) break;
+      int v[kIdGroup];
+#pragma unroll
+      for (int k = 0; k < kIdGroup; ++k) v[k] = (k < gs && lane < nbs[k]) ? __ldg(tbl[k] + js[k] + lane) : 0;
+#pragma unroll
+      for (int k = 0; k < kIdGroup; ++k) {
+        if (k < gs) {
+          const int slot = (g + k) % kIdSlots;
+          mbar_wait(ide0 + 8 * slot, (((g + k) / kIdSlots) & 1) ^ 1);
+          ids[slot * kMaxIds + lane] = v[k];
+          __syncwarp();
+          if (lane == 0) mbar_arrive(idf0 + 8 * slot);
+        }
+      }
+      g += gs;
+    }
+  } else if (warp >= 4 && warp < 4 + kLoadWarps) {
+    // ---- K gather by the loader warps: rows through the block table (ids from the walker), 16-B
+    // cp.async each (D/8 threads per 2*D-byte row, coalesced), written straight into the SW128
+    // K-major layout; the stage's mbarrier counts every thread once its copies land. Step k+ST
+    // is issued right after acc_full(k) proved MMA(k) -- the last reader of stage k%ST -- done.
+    constexpr int CPR = D / 8;                       // 16-B chunks per row
+    constexpr int RPP = kLoadWarps * 32 / CPR;       // rows per pass
+    const int et = threadIdx.x - 4 * 32;
+    const int cr = et % CPR, rsub = et / CPR;
+    const uint32_t chunk_off = (uint32_t)(cr >> 3) * K::SLAB_K;
+    const uint16_t* Kg = reinterpret_cast<const uint16_t*>(c.k_cache);
+    const uint32_t ids_base = smem_u32(ids);
+    const bool b_pow2 = (c.b & (c.b - 1)) == 0;
+    const int b_log2 = 31 - __clz(c.b);
+    // load cursor (may run ahead into the next units); the tile's block ids come from the walker
+    int ld_unit = cluster_id, ld_i = 0, ld_step = 0;
+    UnitInfo ld_u = ld_unit < units ? unit_info(ld_unit) : UnitInfo{};
+    // per-thread constants of the gather: rows RPP*k + rsub, 16-B chunk cr; (row & 7) == (rsub & 7)
+    // because RPP is a multiple of 8, so the SW128 swizzle term is constant per thread
+    const uint32_t dst_thr = (uint32_t)rsub * 128u + (uint32_t)(((cr & 7) ^ (rsub & 7)) << 4) + chunk_off;
+    const uint32_t hD = (uint32_t)c.h_kv * D;              // elements between consecutive slots
+    auto issue_next_load = [&]() {
+      while (ld_unit < units && ld_i >= 2 * ld_u.nt) {
+        ld_unit += nclusters;
+        ld_i = 0;
+        if (ld_unit < units) ld_u = unit_info(ld_unit);
+      }
+      if (ld_unit >= units) return;
+      const int st = ld_step % K::ST;
+      const int slot = ld_step % kIdSlots;
+      const int t0 = tile_of(ld_u, ld_i) * kTile;
+      const int j0 = b_pow2 ? (t0 >> b_log2) : t0 / c.b;
+      const int T = ld_u.T;
+      // 64-bit base of (layer, head, chunk); per-row offsets fit 32 bits (one layer < 2^31 elements)
+      const uint16_t* lbase = Kg + (size_t)ld_u.l * c.N_total * c.b * hD + (size_t)ld_u.h * D + cr * 8;
+      const uint32_t dst0 = smem_u32(Ks + st * K::STAGE_BYTES) + dst_thr;
+      if ((c.debug & 1u) && blockIdx.x == 0 && lane == 0 && ld_step < 256)
+        reinterpret_cast<unsigned long long*>(c.ws.kept)[4096 + ld_step * 16 + (warp - 4)] = gtimer();
+      if ((c.debug & 1u) && blockIdx.x == 0 && et == 0 && ld_step < 512)
+        reinterpret_cast<unsigned long long*>(c.ws.kept)[ld_step * 4 + 0] = gtimer();
+      mbar_wait(idf0 + 8 * slot, (ld_step / kIdSlots) & 1);
+      // all block ids first (explicit ld.shared: a generic load would queue behind the copies)
+      const uint32_t sid = ids_base + (uint32_t)slot * kMaxIds * 4;
+      uint32_t off[kTile / RPP];
+#pragma unroll
+      for (int k = 0; k < kTile / RPP; ++k) {
+        const int t = t0 + RPP * k + rsub;
+        const int jr = b_pow2 ? (t >> b_log2) : t / c.b;
+        const int blk = lds_s32(sid + 4u * (uint32_t)min(max(jr - j0, 0), kMaxIds - 1));
+        off[k] = ((uint32_t)blk * (uint32_t)c.b + (uint32_t)(t - jr * c.b)) * hD;
+      }
+#pragma unroll
+      for (int k = 0; k < kTile / RPP; ++k)
+        if (t0 + RPP * k + rsub < T) cp_async16(dst0 + (uint32_t)(RPP * k * 128), lbase + off[k], 0);
+      cp_async_arrive_noinc(full0 + 8 * st);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(ide0 + 8 * slot);
+      if ((c.debug & 1u) && blockIdx.x == 0 && lane == 0 && ld_step < 256)
+        reinterpret_cast<unsigned long long*>(c.ws.kept)[4096 + ld_step * 16 + 8 + (warp - 4)] = gtimer();
+      ++ld_i;
+      ++ld_step;
+    };
+    for (int g = 0; ; ++g) {
+      if (ld_unit >= units) break;
+      if (g >= K::ST) {   // stage reuse: wait for the MMAs that read it
+        const int st = g % K::ST;
+        mbar_wait(empty0 + 8 * st, ((g / K::ST) & 1) ^ 1);
+      }
+      issue_next_load();
+    }
+
   } else if (warp == 1) {
     // ================= MMA issuer (single thread)
-    if (C > 1) cluster_arrive_relaxed();
     if (lane == 0) {
-      const uint32_t qb = smem_u32(Qs);
-      for (int i = 0; i < 2 * nt; ++i) {
-        const int s = i % kStages, a = i & 1;
-        mbar_wait(acce0 + 8 * a, ((i >> 1) & 1) ^ 1);
-        mbar_wait(full0 + 8 * s, (i / kStages) & 1);
-        tc_fence_after();
-        const uint32_t kb = smem_u32(Ks + s * K::STAGE_BYTES);
-        const uint32_t dacc = tmem + a * 256;
-        if (i < nt) {
+      int kstep = 0, astep = 0;
+      for (int it = 0, unit = cluster_id; unit < units; ++it, unit += nclusters) {
+        const UnitInfo u = unit_info(unit);
+        const int qb = 0;
+        mbar_wait(qfull0, it & 1);
+        const uint32_t qbase = smem_u32(smem + K::OFF_Q0);
+        for (int i = 0; i < 2 * u.nt; ++i, ++kstep, ++astep) {
+          const int s = kstep % K::ST, a = astep & 1;
+          mbar_wait(acce0 + 8 * a, ((astep >> 1) & 1) ^ 1);
+          mbar_wait(full0 + 8 * s, (kstep / K::ST) & 1);
+          if ((c.debug & 1u) && blockIdx.x == 0 && kstep < 512)
+            reinterpret_cast<unsigned long long*>(c.ws.kept)[kstep * 4 + 1] = gtimer();
+          if (!(c.debug & 16u)) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // cp.async data -> tensor core
+          tc_fence_after();
+          const uint32_t kb = smem_u32(Ks + s * K::STAGE_BYTES);
+          const uint32_t dacc = tmem + a * 256;
+          if (c.debug & 4u) {
+            // debug: no MMA
+          } else if (i < u.nt) {
 #pragma unroll
-          for (int half = 0; half < K::M1H; ++half)
+            for (int half = 0; half < K::M1H; ++half)
+#pragma unroll
+              for (int k = 0; k < K::KSTEPS; ++k) {
+                const uint64_t ad = sw128_desc(qbase + (k >> 2) * K::SLAB_Q + half * 128 * 128 + (k & 3) * 32);
+                const uint64_t bd = sw128_desc(kb + (k >> 2) * K::SLAB_K + (k & 3) * 32);
+                umma(dacc + half * 128, ad, bd, idesc_bf16(128, kTile), k > 0);
+              }
+          } else {
 #pragma unroll
             for (int k = 0; k < K::KSTEPS; ++k) {
-              const uint64_t ad = sw128_desc(qb + (k >> 2) * K::SLAB_Q + half * 128 * 128 + (k & 3) * 32);
-              const uint64_t bd = sw128_desc(kb + (k >> 2) * K::SLAB_K + (k & 3) * 32);
-              umma(dacc + half * 128, ad, bd, idesc_bf16(128, kTile), k > 0);
+              const uint64_t ad = sw128_desc(kb + (k >> 2) * K::SLAB_K + (k & 3) * 32);
+              const uint64_t bd = sw128_desc(qbase + (k >> 2) * K::SLAB_Q + (k & 3) * 32);
+              umma(dacc, ad, bd, idesc_bf16(kTile, K::GW), k > 0);
             }
-        } else {
-#pragma unroll
-          for (int k = 0; k < K::KSTEPS; ++k) {
-            const uint64_t ad = sw128_desc(kb + (k >> 2) * K::SLAB_K + (k & 3) * 32);
-            const uint64_t bd = sw128_desc(qb + (k >> 2) * K::SLAB_Q + (k & 3) * 32);
-            umma(dacc, ad, bd, idesc_bf16(kTile, K::GW), k > 0);
           }
+          umma_commit(empty0 + 8 * s);   // K stage s free once these MMAs complete
+          if (c.debug & 8u) mbar_arrive(accf0 + 8 * a);
+          else umma_commit(accf0 + 8 * a);
         }
-        umma_commit(empty0 + 8 * s);
-        umma_commit(accf0 + 8 * a);
+        umma_commit(qempty0 + 8 * qb);     // Q buffer free once this unit's MMAs complete
       }
     }
     __syncwarp();
-    if (C > 1) cluster_wait();
-  } else {
-    // ================= epilogue warps
-    const int ew = warp - 2;
-    const int q = warp & 3;                 // TMEM lane quarter this warp may access
+  } else if (warp >= kEpiWarp0) {
+    // ================= epilogue warps (8): two per TMEM lane quarter
+    const int ew = warp - kEpiWarp0;
+    const int q = warp & 3;
     const int half = ew >> 2;
     const int col = half * 128 + q * 32 + lane;
     const bool warp_cols = (half * 128 + q * 32) < K::GW;
     const bool col_ok = col < K::GW;
     const int u1 = col_ok ? col / G : 0;
-    const int limit1 = T - W + u1;          // pass-1 causal limit of this column (R1, R2)
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
-    float m = -INFINITY, ssum = 0.f;
-    for (int i = 0; i < 2 * nt; ++i) {
-      const int a = i & 1;
-      mbar_wait(accf0 + 8 * a, (i >> 1) & 1);
-      tc_fence_after();
-      const int t0 = (tb + i % nt) * kTile;
-      if (i < nt) {
-        // ---- pass 1: this thread owns window column `col`; 128 token logits in TMEM columns,
-        //      consumed as two 64-column batches with an online (max, sum) update.
-#pragma unroll 1
-        for (int bh = 0; bh < 2; ++bh) {
-          float v[64];
-          if (warp_cols) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) TMEM_LD16(lane_base + a * 256 + half * 128 + bh * 64 + k * 16, v, k * 16);
-            tmem_wait_ld();
-          }
-          if (bh == 1) {
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(acce0 + 8 * a);
-          }
-          if (col_ok) {
-            const int tbase = t0 + bh * 64;
-            if (tbase + 63 > limit1) {
-#pragma unroll
-              for (int j = 0; j < 64; ++j)
-                if (tbase + j > limit1) v[j] = -INFINITY;
+
+    int astep = 0;
+    for (int it = 0, unit = cluster_id; unit < units; ++it, unit += nclusters) {
+      const UnitInfo u = unit_info(unit);
+      const int limit1 = u.T - W + u1;   // pass-1 causal limit of this column (R1, R2)
+      float m = -INFINITY, ssum = 0.f;
+      for (int i = 0; i <= 2 * u.nt; ++i) {
+        if (i == u.nt) {
+          // ---- end of pass 1: LSE per column, combined across the cluster through DSMEM
+          const int pb = it & 1;
+          if (C == 1) {
+            if (col_ok) {
+              const float L2 = m + lg2f(ssum);
+              negL[col] = -L2;
+              c.ws.lse[(size_t)unit * K::GW + col] = L2;
             }
-            float mp[8];
+          } else {
+            if (col_ok) { pmv[pb * 256 + col] = m; psv[pb * 256 + col] = ssum; }
+            named_bar(1, kEpiWarps * 32);
+            if (ew == 0 && lane == 0) {
+              asm volatile("fence.acq_rel.cluster;" ::: "memory");
 #pragma unroll
-            for (int j = 0; j < 8; ++j) mp[j] = v[j];
+              for (int rr = 0; rr < C; ++rr) mbar_remote_arrive(xchg0 + 8 * pb, rr);
+            }
+            mbar_wait_cluster(xchg0 + 8 * pb, (it >> 1) & 1);
+            if (col_ok) {
+              float M = -INFINITY, mr[C], sr[C];
 #pragma unroll
-            for (int j = 8; j < 64; ++j) mp[j & 7] = fmaxf(mp[j & 7], v[j]);
-            const float mx = fmaxf(fmaxf(fmaxf(mp[0], mp[1]), fmaxf(mp[2], mp[3])),
-                                   fmaxf(fmaxf(mp[4], mp[5]), fmaxf(mp[6], mp[7])));
-            if (mx > -INFINITY) {
-              const float mn = fmaxf(m, mx * scale);
-              float sp[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-              for (int j = 0; j < 64; ++j) {
-                const float arg = fmaf(v[j], scale, -mn);
-                sp[j & 3] += (kPolyEvery > 0 && (j % kPolyEvery) == kPolyEvery - 1) ? ex2_poly(arg) : ex2f(arg);
+              for (int rr = 0; rr < C; ++rr) {
+                mr[rr] = ld_dsmem_f32(pmv + pb * 256 + col, rr);
+                sr[rr] = ld_dsmem_f32(psv + pb * 256 + col, rr);
+                M = fmaxf(M, mr[rr]);
               }
-              ssum = (m > -INFINITY ? ssum * ex2f(m - mn) : 0.f) + ((sp[0] + sp[1]) + (sp[2] + sp[3]));
-              m = mn;
+              float S = 0.f;
+#pragma unroll
+              for (int rr = 0; rr < C; ++rr)
+                if (mr[rr] > -INFINITY) S += sr[rr] * ex2f(mr[rr] - M);
+              const float L2 = M + lg2f(S);
+              negL[col] = -L2;
+              if (rank == 0) c.ws.lse[(size_t)unit * K::GW + col] = L2;
             }
           }
+          named_bar(1, kEpiWarps * 32);
+          if (i == 2 * u.nt) break;
+          continue;
         }
-      } else {
-        // ---- pass 2: this thread owns token t0 + q*32 + lane and the window rows of its half;
-        //      columns stream in batches of <= 64; (u, g) of every column is a compile-time constant.
-        const int t = t0 + q * 32 + lane;
-        const int du = t - (T - W) - half * (W / 2);   // window row uu of this half is causal iff uu >= du
-        const float4* nl4 = reinterpret_cast<const float4*>(negL + half * K::HC);
-        float acc0 = 0.f, acc1 = 0.f, mx = 0.f;
-        constexpr int NCH = K::HC / 16;
+        const int a = astep & 1;
+        if (!(c.debug & 64u)) mbar_wait(accf0 + 8 * a, (astep >> 1) & 1);
+        tc_fence_after();
+        if ((c.debug & 1u) && blockIdx.x == 0 && ew == 0 && lane == 0 && astep < 512)
+          reinterpret_cast<unsigned long long*>(c.ws.kept)[astep * 4 + 2] = gtimer();
+        const int t0 = tile_of(u, i < u.nt ? i : i - 1) * kTile;
+        if (c.debug & 2u) {
+          // debug: no epilogue math
+          __syncwarp();
+          if (lane == 0) mbar_arrive(acce0 + 8 * a);
+        } else if (i < u.nt) {
+          // ---- pass 1: this thread owns window column `col`; two 64-token batches
+#pragma unroll 1
+          for (int bh = 0; bh < 2; ++bh) {
+            float v[64];
+            if (warp_cols) {
 #pragma unroll
-        for (int b0 = 0; b0 < NCH; b0 += 4) {
-          float v[64];
+              for (int k = 0; k < 4; ++k) TMEM_LD16(lane_base + a * 256 + half * 128 + bh * 64 + k * 16, v, k * 16);
+              tmem_wait_ld();
+            }
+            if (bh == 1) {
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(acce0 + 8 * a);
+            }
+            if (col_ok) {
+              const int tbase = t0 + bh * 64;
+              if (tbase + 63 > limit1) {
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            if (b0 + k < NCH) TMEM_LD16(lane_base + a * 256 + half * K::HC + (b0 + k) * 16, v, k * 16);
-          tmem_wait_ld();
-          if (b0 + 4 >= NCH) {
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(acce0 + 8 * a);
-          }
+                for (int j = 0; j < 64; ++j)
+                  if (tbase + j > limit1) v[j] = -INFINITY;
+              }
+              // running reference m (no per-batch max): exact re-run only when the batch sum could
+              // overflow (first batch: m = -inf -> NaN/inf -> re-run)
+              float bsum = sum_exp64(v, scale, m);
+              if (!(bsum < 1.8446744e19f)) {
+                float mp[8];
 #pragma unroll
-          for (int j4 = 0; j4 < 16; ++j4) {
-            if (b0 * 16 + j4 * 4 < K::HC) {
-              const float4 L4 = nl4[b0 * 4 + j4];
-              const float Lv[4] = {L4.x, L4.y, L4.z, L4.w};
+                for (int j = 0; j < 8; ++j) mp[j] = v[j];
 #pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const int cc = b0 * 16 + j4 * 4 + e;      // column within the half (compile time)
-                const int uu = cc / G, g = cc % G;
-                const float y = fmaf(v[j4 * 4 + e], scale, Lv[e]);
-                mx = (g == 0) ? y : fmaxf(mx, y);
-                if (g == G - 1) {
-                  const float pterm = (uu >= du) ? ex2f(mx) : 0.f;
-                  if (uu & 1) acc1 += pterm; else acc0 += pterm;
+                for (int j = 8; j < 64; j += 2) mp[(j >> 1) & 7] = max3f(mp[(j >> 1) & 7], v[j], v[j + 1]);
+                const float mx = fmaxf(max3f(mp[0], mp[1], mp[2]), max3f(max3f(mp[3], mp[4], mp[5]), mp[6], mp[7]));
+                if (mx > -INFINITY) {
+                  const float mn = fmaxf(m, mx * scale);
+                  ssum = (m > -INFINITY) ? ssum * ex2f(m - mn) : 0.f;
+                  m = mn;
+                  bsum = sum_exp64(v, scale, m);
+                } else {
+                  bsum = 0.f;
                 }
               }
+              ssum += bsum;
             }
-          }
-        }
-        const float acc = acc0 + acc1;
-        float* cb = comb + (i & 1) * kTile;
-        if (half == 1) cb[q * 32 + lane] = acc;
-        named_bar(1, kEpiWarps * 32);
-        if (half == 0 && t < T)
-          c.ws.scores[(size_t)unit * c.max_seq_len + t] = (acc + cb[q * 32 + lane]) * (1.0f / W);
-      }
-      if (i == nt - 1) {
-        // ---- end of pass 1: LSE per column (combined across the cluster through DSMEM)
-        if (C == 1) {
-          if (col_ok) {
-            const float L2 = m + lg2f(ssum);
-            negL[col] = -L2;
-            c.ws.lse[(size_t)unit * K::GW + col] = L2;
           }
         } else {
-          if (col_ok) { pm[col] = m; ps[col] = ssum; }
-          cluster_arrive_release();
-          cluster_wait();
-          if (col_ok) {
-            float M = -INFINITY;
+          // ---- pass 2: this thread owns token t; the W/2 window rows of its half in batches of
+          //      UB rows (UB*G columns, loaded from TMEM in 16-column chunks, LSE as float4)
+          const int t = t0 + q * 32 + lane;
+          const int du = t - (u.T - W) - half * (W / 2);   // row uu of this half is causal iff uu >= du
+          float acc0 = 0.f, acc1 = 0.f;
 #pragma unroll
-            for (int rr = 0; rr < C; ++rr) M = fmaxf(M, ld_dsmem_f32(pm + col, rr));
-            float S = 0.f;
+          for (int bb = 0; bb < (W / 2) / K::UB; ++bb) {
+            constexpr int BC = K::UB * G;                   // columns per batch
+            const int c0 = bb * BC;                         // first column of the batch (in half)
+            const int l0 = (c0 / 16) * 16;                  // 16-aligned TMEM load window
+            const int nld = (c0 + BC - l0 + 15) / 16;
+            float v[K::LDMAX * 16];
 #pragma unroll
-            for (int rr = 0; rr < C; ++rr) {
-              const float mr = ld_dsmem_f32(pm + col, rr);
-              if (mr > -INFINITY) S += ld_dsmem_f32(ps + col, rr) * ex2f(mr - M);
+            for (int k = 0; k < K::LDMAX; ++k)
+              if (k < nld) TMEM_LD16(lane_base + a * 256 + half * K::HC + l0 + k * 16, v, k * 16);
+            float Lv[BC];
+            const float4* L4 = reinterpret_cast<const float4*>(negL + half * K::HC + c0);
+#pragma unroll
+            for (int j = 0; j < BC / 4; ++j) {
+              const float4 x = L4[j];
+              Lv[4 * j] = x.x; Lv[4 * j + 1] = x.y; Lv[4 * j + 2] = x.z; Lv[4 * j + 3] = x.w;
             }
-            const float L2 = M + lg2f(S);
-            negL[col] = -L2;
-            if (rank == 0) c.ws.lse[(size_t)unit * K::GW + col] = L2;
+            tmem_wait_ld();
+            if (bb == (W / 2) / K::UB - 1) {
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(acce0 + 8 * a);
+            }
+#pragma unroll
+            for (int uu = 0; uu < K::UB; ++uu) {
+              const int o = c0 - l0 + uu * G;
+              float mx = fmaf(v[o], scale, Lv[uu * G]);
+#pragma unroll
+              for (int g = 1; g < G; g += 2)
+                mx = (g + 1 < G) ? max3f(mx, fmaf(v[o + g], scale, Lv[uu * G + g]),
+                                         fmaf(v[o + g + 1], scale, Lv[uu * G + g + 1]))
+                                 : fmaxf(mx, fmaf(v[o + g], scale, Lv[uu * G + g]));
+              const float pterm = (bb * K::UB + uu >= du) ? ex2f(mx) : 0.f;
+              if (uu & 1) acc1 += pterm; else acc0 += pterm;
+            }
           }
+          const float acc = acc0 + acc1;
+          float* cb = comb + (astep & 1) * kTile;
+          if (half == 1) cb[q * 32 + lane] = acc;
+          named_bar(1, kEpiWarps * 32);
+          if (half == 0 && t < u.T)
+            c.ws.scores[(size_t)unit * c.max_seq_len + t] = (acc + cb[q * 32 + lane]) * (1.0f / W);
         }
-        named_bar(1, kEpiWarps * 32);
+        ++astep;
       }
-    }
-    if (nt == 0 && C > 1) {
-      // this CTA got no tiles: publish an empty partial and take part in the exchange
-      if (col_ok) { pm[col] = -INFINITY; ps[col] = 0.f; }
-      cluster_arrive_release();
-      cluster_wait();
     }
   }
   // ---- teardown
@@ -442,10 +717,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
   tc_fence_after();
   if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
-  if (C > 1) {
-    cluster_arrive_release();   // no CTA leaves while a peer may still read its pm/ps
-    cluster_wait();
-  }
+  if (C > 1) cluster_sync_all();   // no CTA leaves while a peer may still read its partials
 }
 
 // ------------------------------------------------------------------ host side
@@ -466,14 +738,14 @@ EncodeTiledFn encode_fn() {
 }
 
 template <int G, int W, int D, int C>
-cudaError_t launch_tc(const Call& c, const CUtensorMap& tm, cudaStream_t s) {
+cudaError_t launch_tc(const Call& c, const CUtensorMap& tq, cudaStream_t s) {
   using K = Cfg<G, W, D, C>;
   auto kern = k_score_tc<G, W, D, C>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K::SMEM);
   if (e != cudaSuccess) return e;
+  if (C > 1) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
   const int units = c.R * c.L * c.h_kv;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(units * C);
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = K::SMEM;
   cfg.stream = s;
@@ -484,64 +756,71 @@ cudaError_t launch_tc(const Call& c, const CUtensorMap& tm, cudaStream_t s) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, c, tm);
+  // persistent: as many clusters as can be co-resident (one CTA per SM), each looping over units
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int max_clusters = sms / C;
+  cfg.gridDim = dim3(C);
+  int q = 0;
+  if (cudaOccupancyMaxActiveClusters(&q, kern, &cfg) == cudaSuccess && q > 0) max_clusters = q;
+  cudaGetLastError();
+  cfg.gridDim = dim3((unsigned)(std::min(units, max_clusters) * C));
+  return cudaLaunchKernelEx(&cfg, kern, c, tq);
 }
 
 // Cluster size: CTAs per unit. Splitting a unit's tokens over C CTAs shrinks the K slice each
 // CTA re-reads in pass 2 (in flight across the GPU: ~148/C slices), keeping it L2-resident
-// (DESIGN.md §Score kernel, L2 reuse). ZPC_SCORE_CLUSTER (1/2/4) overrides, for tuning runs.
+// (DESIGN.md §Score kernel, L2 reuse). ZPC_SCORE_CLUSTER (1/2) overrides, for tuning runs.
 int cluster_size(const Call& c) {
   if (const char* e = getenv("ZPC_SCORE_CLUSTER")) {
     const int v = atoi(e);
-    if (v == 1 || v == 2 || v == 4) return v;
+    if (v == 1 || v == 2) return v;
   }
-  if (c.max_seq_len < 2 * kTile) return 1;
-  if (c.max_seq_len < 16 * kTile) return 2;
-  return 4;
+  return c.max_seq_len < 2 * kTile ? 1 : 2;
 }
 
 template <int G, int W, int D>
-cudaError_t launch_c(const Call& c, const CUtensorMap& tm, cudaStream_t s) {
-  switch (cluster_size(c)) {
-    case 4: return launch_tc<G, W, D, 4>(c, tm, s);
-    case 2: return launch_tc<G, W, D, 2>(c, tm, s);
-    default: return launch_tc<G, W, D, 1>(c, tm, s);
-  }
+cudaError_t launch_c(const Call& c, const CUtensorMap& tq, cudaStream_t s) {
+  return cluster_size(c) == 2 ? launch_tc<G, W, D, 2>(c, tq, s) : launch_tc<G, W, D, 1>(c, tq, s);
 }
 
 template <int D>
-cudaError_t dispatch_g(const Call& c, const CUtensorMap& tm, cudaStream_t s, bool* used) {
+cudaError_t dispatch_g(const Call& c, const CUtensorMap& tq, cudaStream_t s, bool* used) {
   if (c.w != 32) return cudaSuccess;
   *used = true;
   switch (c.G) {
-    case 4: return launch_c<4, 32, D>(c, tm, s);
-    case 5: return launch_c<5, 32, D>(c, tm, s);
-    case 7: return launch_c<7, 32, D>(c, tm, s);
-    case 8: return launch_c<8, 32, D>(c, tm, s);
+    case 4: return launch_c<4, 32, D>(c, tq, s);
+    case 5: return launch_c<5, 32, D>(c, tq, s);
+    case 7: return launch_c<7, 32, D>(c, tq, s);
+    case 8: return launch_c<8, 32, D>(c, tq, s);
     default: *used = false; return cudaSuccess;
   }
 }
 
 }  // namespace
 
-cudaError_t launch_score_tc(const Call& c, cudaStream_t s, bool* used) {
+cudaError_t launch_score_tc(const Call& c_in, cudaStream_t s, bool* used) {
   *used = false;
+  Call c = c_in;
+  if (const char* e = getenv("ZPC_SCORE_DEBUG")) c.debug = (uint32_t)strtoul(e, nullptr, 10);   // tuning runs only
   if (c.dtype != ZPC_BF16) return cudaSuccess;
-  const bool b_ok = (c.b >= 8 && kTile % c.b == 0) || (c.b % kTile == 0);
-  if (!b_ok || (c.d != 64 && c.d != 128)) return cudaSuccess;
+  if (c.d != 64 && c.d != 128) return cudaSuccess;
+  if (c.b < 5) return cudaSuccess;   // a 128-token tile must span <= kMaxIds blocks
   if (c.R * c.L * c.h_kv == 0) { *used = true; return cudaSuccess; }
   EncodeTiledFn enc = encode_fn();
   if (!enc) return cudaSuccess;
-  CUtensorMap tm;
-  const cuuint64_t gdim[3] = {(cuuint64_t)c.d, (cuuint64_t)c.h_kv, (cuuint64_t)c.L * c.N_total * c.b};
-  const cuuint64_t gstride[2] = {(cuuint64_t)c.d * 2, (cuuint64_t)c.h_kv * c.d * 2};
-  const cuuint32_t box[3] = {64, 1, (cuuint32_t)(c.b >= kTile ? kTile : c.b)};
   const cuuint32_t estr[3] = {1, 1, 1};
-  CUresult cr = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, c.k_cache, gdim, gstride, box, estr,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (cr != CUDA_SUCCESS) return cudaSuccess;   // not expressible as a tensor map: CUDA-core path
-  return c.d == 64 ? dispatch_g<64>(c, tm, s, used) : dispatch_g<128>(c, tm, s, used);
+  // Q cache viewed as [rows = L*M*w][h_q][d]; one box = the unit's G heads x w window rows
+  CUtensorMap tq;
+  const cuuint64_t qdim[3] = {(cuuint64_t)c.d, (cuuint64_t)c.h_q, (cuuint64_t)c.L * c.M * c.w};
+  const cuuint64_t qstr[2] = {(cuuint64_t)c.d * 2, (cuuint64_t)c.h_q * c.d * 2};
+  const cuuint32_t qbox[3] = {64, (cuuint32_t)c.G, (cuuint32_t)c.w};
+  if (enc(&tq, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(c.q_cache), qdim, qstr, qbox, estr,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return cudaSuccess;   // not expressible as a tensor map: CUDA-core path
+  return c.d == 64 ? dispatch_g<64>(c, tq, s, used) : dispatch_g<128>(c, tq, s, used);
 }
 
 }  // namespace zpc
