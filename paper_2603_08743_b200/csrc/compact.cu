@@ -1,23 +1,55 @@
 // a5: in-place compaction of kept K/V rows (Alg. 4), one CTA per unit (r, l, h).
 //
 // Alg. 4 is a sequential two-pointer sweep; here rank i of the ascending kept list moves
-// row kept[i] -> target slot i. Hazard argument: kept[i] >= i, and a
-// destination aliases a source only when both are the same logical position of an own target
-// block, i.e. i == kept[i] (skipped as an identity move). Processing ranks in ascending chunks
-// of kChunk rows, with every read of a chunk completed (CTA barrier) before any write of it,
-// is therefore hazard-free: writes of chunk j land on logical positions < (j+1)*kChunk, below
-// every source of chunks > j. Rows move as 16-byte vectors, coalesced along d.
+// row kept[i] -> target slot i. Hazard argument: kept[i] >= i, and a destination
+// aliases a source only when both are the same logical position of an own target block, i.e.
+// i == kept[i] (skipped as an identity move). Ranks are processed in ascending chunks of kChunk
+// rows with every read of a chunk completed (CTA barrier) before any write of it; the writes of
+// chunk j land on logical positions < (j+1)*kChunk, below every source of chunks > j, so the
+// loads of chunk j+1 may be issued before the stores of chunk j (software pipelining).
+// Rows move as 16-byte vectors, coalesced along d.
 #include "internal.h"
 
 namespace zpc {
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kChunk = 64;           // rows per chunk
+constexpr int kThreads = 128;
+constexpr int kChunk = 16;           // rows per chunk
 constexpr int kMaxVecPerRow = 32;    // d*e/16 <= 32 (fp32, d=128)
 constexpr int kRegs = kChunk * kMaxVecPerRow / kThreads;   // 8 int4 per tensor per thread
 
-__global__ void __launch_bounds__(kThreads) k_compact(Call c) {
+struct Chunk {
+  int4 k[kRegs], v[kRegs];
+  uint32_t dst[kRegs];               // destination vector index within the layer-head plane, ~0u = none
+};
+
+__device__ __forceinline__ void load_chunk(const Call& c, Chunk& ch, int base, int ell, int vpr, const int32_t* kept,
+                                           const int32_t* table, const int32_t* tg, const int4* K, const int4* V,
+                                           size_t plane, int esz) {
+  const int rows = min(kChunk, ell - base);
+  const int nvec = rows * vpr;
+#pragma unroll
+  for (int k = 0; k < kRegs; ++k) {
+    const int v = threadIdx.x + k * kThreads;
+    ch.dst[k] = ~0u;
+    if (v < nvec) {
+      const int i = base + v / vpr, e = v % vpr;
+      const int t = kept[i];
+      const int sblk = table[t / c.b], dblk = tg[i / c.b];
+      // vector index relative to (layer, head) plane: ((blk*b + slot)*h_kv)*vpr + e
+      const uint32_t src = (uint32_t)(((size_t)sblk * c.b + t % c.b) * c.h_kv * vpr + e);
+      const uint32_t d = (uint32_t)(((size_t)dblk * c.b + i % c.b) * c.h_kv * vpr + e);
+      if (src != d) {
+        ch.k[k] = K[plane + src];
+        ch.v[k] = V[plane + src];
+        ch.dst[k] = d;
+      }
+    }
+  }
+  (void)esz;
+}
+
+__global__ void __launch_bounds__(kThreads, 6) k_compact(Call c) {
   if (*c.status != ZPC_OK) return;
   const int unit = blockIdx.x;
   const int h = unit % c.h_kv;
@@ -34,42 +66,26 @@ __global__ void __launch_bounds__(kThreads) k_compact(Call c) {
   const int4* V = reinterpret_cast<const int4*>(c.v_cache);
   int4* Kw = reinterpret_cast<int4*>(c.k_cache);
   int4* Vw = reinterpret_cast<int4*>(c.v_cache);
-  const size_t row_vecs = (size_t)vpr;
+  // start of the (layer l, head h) plane in vectors; per-row offsets are 32-bit within a layer
+  const size_t plane = (size_t)l * c.N_total * c.b * c.h_kv * vpr + (size_t)h * vpr;
   unsigned moved = 0;
 
+  Chunk cur, nxt;
+  if (ell > 0) load_chunk(c, cur, 0, ell, vpr, kept, table, tg, K, V, plane, esz);
   for (int base = 0; base < ell; base += kChunk) {
-    int4 kb[kRegs], vb[kRegs];
-    size_t dst[kRegs];
-    const int rows = min(kChunk, ell - base);
-    const int nvec = rows * vpr;
+    __syncthreads();   // every read of chunk `base` has returned before any write of it
+    const bool more = base + kChunk < ell;
+    if (more) load_chunk(c, nxt, base + kChunk, ell, vpr, kept, table, tg, K, V, plane, esz);
 #pragma unroll
     for (int k = 0; k < kRegs; ++k) {
-      const int v = threadIdx.x + k * kThreads;
-      dst[k] = (size_t)-1;
-      if (v < nvec) {
-        const int i = base + v / vpr, e = v % vpr;
-        const int t = kept[i];
-        const int sblk = table[t / c.b], dblk = tg[i / c.b];
-        const size_t src = kv_row(c, l, sblk, t % c.b, h) * esz / 16 + e;
-        const size_t d = kv_row(c, l, dblk, i % c.b, h) * esz / 16 + e;
-        if (src != d) {
-          kb[k] = K[src];
-          vb[k] = V[src];
-          dst[k] = d;
-        }
-      }
-    }
-    __syncthreads();   // all reads of this chunk precede any write of it
-#pragma unroll
-    for (int k = 0; k < kRegs; ++k) {
-      if (dst[k] != (size_t)-1) {
-        Kw[dst[k]] = kb[k];
-        Vw[dst[k]] = vb[k];
+      if (cur.dst[k] != ~0u) {
+        Kw[plane + cur.dst[k]] = cur.k[k];
+        Vw[plane + cur.dst[k]] = cur.v[k];
         moved += ((threadIdx.x + k * kThreads) % vpr) == 0;
       }
     }
+    if (more) cur = nxt;
   }
-  (void)row_vecs;
   if (c.flags & ZPC_F_COUNT_MOVES) {
     for (int o = 16; o; o >>= 1) moved += __shfl_xor_sync(0xffffffffu, moved, o);
     if ((threadIdx.x & 31) == 0 && moved) atomicAdd(c.ws.moves, (unsigned long long)moved);

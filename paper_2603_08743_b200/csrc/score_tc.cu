@@ -33,6 +33,7 @@ constexpr int kTile = 128;       // tokens per tile (UMMA M in pass 2, N in pass
 constexpr int kThreads = 512;    // 16 warps: Q-TMA, MMA, table walker, spare, 4 K loaders, 8 epilogue
 constexpr int kLoadWarps = 4;
 constexpr int kEpiWarp0 = 8;     // first epilogue warp (warps 8..15: lane quarter = warp % 4)
+constexpr bool kPolyOffload = false;   // 25% of pass-1 exp2 on the FMA pipe (pays off only when MUFU-bound)
 constexpr int kIdSlots = 8;      // block-id ring (steps) filled by the walker, 4 steps per group
 constexpr int kIdGroup = 4;
 constexpr int kMaxIds = 32;      // block ids per 128-token tile (b >= 5)
@@ -274,7 +275,7 @@ struct Cfg {
 // 2^x on MUFU for most pairs, on the FMA pipe for pairs j % 4 == 3 (25%): balances the two pipes.
 template <int J>
 __device__ __forceinline__ uint64_t ex2_pair(uint64_t a2) {
-  if constexpr ((J & 3) == 3) {
+  if constexpr (kPolyOffload && (J & 3) == 3) {
     return ex2_poly2(a2);
   } else {
     float a0, a1;
@@ -291,6 +292,26 @@ __device__ __forceinline__ void sum_exp_rec(const float* v, uint64_t S2, uint64_
     acc[J & 3] = add2(acc[J & 3], ex2_pair<J>(arg));
     sum_exp_rec<J + 1>(v, S2, NM2, acc);
   }
+}
+template <int N>
+__device__ __forceinline__ float sum_exp_n(const float* v, float scale, float m) {
+  uint64_t acc[4] = {0, 0, 0, 0};
+  const uint64_t S2 = pk2(scale, scale), NM2 = pk2(-m, -m);
+#pragma unroll
+  for (int j = 0; j < N / 2; ++j) {
+    const uint64_t arg = fma2(pk2(v[2 * j], v[2 * j + 1]), S2, NM2);
+    if (kPolyOffload && (j & 3) == 3) {
+      acc[j & 3] = add2(acc[j & 3], ex2_poly2(arg));
+    } else {
+      float a0, a1;
+      upk2(arg, a0, a1);
+      acc[j & 3] = add2(acc[j & 3], pk2(ex2f(a0), ex2f(a1)));
+    }
+  }
+  const uint64_t s2 = add2(add2(acc[0], acc[1]), add2(acc[2], acc[3]));
+  float a, b;
+  upk2(s2, a, b);
+  return a + b;
 }
 __device__ __forceinline__ float sum_exp64(const float* v, float scale, float m) {
   uint64_t acc[4] = {0, 0, 0, 0};
@@ -438,6 +459,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
     // is issued right after acc_full(k) proved MMA(k) -- the last reader of stage k%ST -- done.
     constexpr int CPR = D / 8;                       // 16-B chunks per row
     constexpr int RPP = kLoadWarps * 32 / CPR;       // rows per pass
+    static_assert(RPP % 8 == 0, "the per-thread SW128 swizzle term needs rows-per-pass % 8 == 0");
     const int et = threadIdx.x - 4 * 32;
     const int cr = et % CPR, rsub = et / CPR;
     const uint32_t chunk_off = (uint32_t)(cr >> 3) * K::SLAB_K;
@@ -615,42 +637,47 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
           __syncwarp();
           if (lane == 0) mbar_arrive(acce0 + 8 * a);
         } else if (i < u.nt) {
-          // ---- pass 1: this thread owns window column `col`; two 64-token batches
-#pragma unroll 1
-          for (int bh = 0; bh < 2; ++bh) {
-            float v[64];
-            if (warp_cols) {
+          // ---- pass 1: this thread owns window column `col`; 128 token logits in TMEM, consumed
+          //      as 4 batches of 32 with the next batch's TMEM load in flight during the math
+          constexpr int NB = 32;
+          float vb[2][NB];
+          if (warp_cols) {
+            TMEM_LD16(lane_base + a * 256 + half * 128, vb[0], 0);
+            TMEM_LD16(lane_base + a * 256 + half * 128 + 16, vb[0], 16);
+          }
 #pragma unroll
-              for (int k = 0; k < 4; ++k) TMEM_LD16(lane_base + a * 256 + half * 128 + bh * 64 + k * 16, v, k * 16);
-              tmem_wait_ld();
-            }
-            if (bh == 1) {
+          for (int bh = 0; bh < kTile / NB; ++bh) {
+            float* v = vb[bh & 1];
+            if (warp_cols) tmem_wait_ld();
+            if (bh + 1 < kTile / NB) {
+              if (warp_cols) {
+                TMEM_LD16(lane_base + a * 256 + half * 128 + (bh + 1) * NB, vb[(bh + 1) & 1], 0);
+                TMEM_LD16(lane_base + a * 256 + half * 128 + (bh + 1) * NB + 16, vb[(bh + 1) & 1], 16);
+              }
+            } else {
               tc_fence_before();
               __syncwarp();
               if (lane == 0) mbar_arrive(acce0 + 8 * a);
             }
             if (col_ok) {
-              const int tbase = t0 + bh * 64;
-              if (tbase + 63 > limit1) {
+              const int tbase = t0 + bh * NB;
+              if (tbase + NB - 1 > limit1) {
 #pragma unroll
-                for (int j = 0; j < 64; ++j)
+                for (int j = 0; j < NB; ++j)
                   if (tbase + j > limit1) v[j] = -INFINITY;
               }
               // running reference m (no per-batch max): exact re-run only when the batch sum could
               // overflow (first batch: m = -inf -> NaN/inf -> re-run)
-              float bsum = sum_exp64(v, scale, m);
+              float bsum = sum_exp_n<NB>(v, scale, m);
               if (!(bsum < 1.8446744e19f)) {
-                float mp[8];
+                float mx = v[0];
 #pragma unroll
-                for (int j = 0; j < 8; ++j) mp[j] = v[j];
-#pragma unroll
-                for (int j = 8; j < 64; j += 2) mp[(j >> 1) & 7] = max3f(mp[(j >> 1) & 7], v[j], v[j + 1]);
-                const float mx = fmaxf(max3f(mp[0], mp[1], mp[2]), max3f(max3f(mp[3], mp[4], mp[5]), mp[6], mp[7]));
+                for (int j = 1; j < NB; j += 2) mx = (j + 1 < NB) ? max3f(mx, v[j], v[j + 1]) : fmaxf(mx, v[j]);
                 if (mx > -INFINITY) {
                   const float mn = fmaxf(m, mx * scale);
                   ssum = (m > -INFINITY) ? ssum * ex2f(m - mn) : 0.f;
                   m = mn;
-                  bsum = sum_exp64(v, scale, m);
+                  bsum = sum_exp_n<NB>(v, scale, m);
                 } else {
                   bsum = 0.f;
                 }
@@ -675,12 +702,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
             for (int k = 0; k < K::LDMAX; ++k)
               if (k < nld) TMEM_LD16(lane_base + a * 256 + half * K::HC + l0 + k * 16, v, k * 16);
             float Lv[BC];
-            const float4* L4 = reinterpret_cast<const float4*>(negL + half * K::HC + c0);
+            const uint32_t L4 = smem_u32(negL + half * K::HC + c0);
 #pragma unroll
-            for (int j = 0; j < BC / 4; ++j) {
-              const float4 x = L4[j];
-              Lv[4 * j] = x.x; Lv[4 * j + 1] = x.y; Lv[4 * j + 2] = x.z; Lv[4 * j + 3] = x.w;
-            }
+            for (int j = 0; j < BC / 4; ++j)
+              asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                           : "=f"(Lv[4 * j]), "=f"(Lv[4 * j + 1]), "=f"(Lv[4 * j + 2]), "=f"(Lv[4 * j + 3])
+                           : "r"(L4 + 16u * j));
             tmem_wait_ld();
             if (bb == (W / 2) / K::UB - 1) {
               tc_fence_before();
