@@ -69,6 +69,22 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     if (++spins > (1LL << 22)) __trap();   // a pipeline bug must fail loudly, never hang the GPU
   }
 }
+// for waiters off the critical path: back off between polls so they do not flood the issue
+// slots / instruction cache the MUFU-bound epilogue needs (measured: polls were 19% no_inst)
+__device__ __forceinline__ void mbar_wait_backoff(uint32_t bar, uint32_t parity, int ns) {
+  uint32_t done = 0;
+  long long spins = 0;
+  while (true) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    if (done) return;
+    __nanosleep(ns);
+    if (++spins > (1LL << 24)) __trap();
+  }
+}
 __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2,
                                             uint32_t bar, uint64_t policy) {
   asm volatile(
@@ -156,6 +172,7 @@ __device__ __forceinline__ void umma_commit(uint32_t bar) {
                : "r"(taddr))
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void named_bar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void cluster_arrive_release() {
   asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
 }
@@ -400,7 +417,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
       for (int it = 0, unit = cluster_id; unit < units; ++it, unit += nclusters) {
         const UnitInfo u = unit_info(unit);
         const int qb = 0;                    // single Q buffer (see kL1Reserve)
-        mbar_wait(qempty0, (it & 1) ^ 1);
+        mbar_wait_backoff(qempty0, (it & 1) ^ 1, 2000);
         if (c.debug & 32u) { mbar_arrive(qfull0); continue; }   // bisection: no Q load
         mbar_expect_tx(qfull0, K::Q_BYTES);
         const uint32_t qdst = smem_u32(smem + K::OFF_Q0);
@@ -410,6 +427,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
       }
     }
     __syncwarp();
+  } else if (warp == 2 && (c.debug & 2048u)) {
+    // bisection: no walker
+  } else if (warp >= 4 && warp < 4 + kLoadWarps && (c.debug & 2048u)) {
+    // bisection: no loaders
   } else if (warp == 2) {
     // ================= table walker: block ids of every K tile, kIdGroup steps at a time, into a
     // shared ring, so the gathering threads never wait on a table load (DESIGN.md §Score kernel)
@@ -444,7 +465,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
       for (int k = 0; k < kIdGroup; ++k) {
         if (k < gs) {
           const int slot = (g + k) % kIdSlots;
-          mbar_wait(ide0 + 8 * slot, (((g + k) / kIdSlots) & 1) ^ 1);
+          mbar_wait_backoff(ide0 + 8 * slot, (((g + k) / kIdSlots) & 1) ^ 1, 200);
           ids[slot * kMaxIds + lane] = v[k];
           __syncwarp();
           if (lane == 0) mbar_arrive(idf0 + 8 * slot);
@@ -493,7 +514,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
         reinterpret_cast<unsigned long long*>(c.ws.kept)[4096 + ld_step * 16 + (warp - 4)] = gtimer();
       if ((c.debug & 1u) && blockIdx.x == 0 && et == 0 && ld_step < 512)
         reinterpret_cast<unsigned long long*>(c.ws.kept)[ld_step * 4 + 0] = gtimer();
-      mbar_wait(idf0 + 8 * slot, (ld_step / kIdSlots) & 1);
+      mbar_wait_backoff(idf0 + 8 * slot, (ld_step / kIdSlots) & 1, 100);
       // all block ids first (explicit ld.shared: a generic load would queue behind the copies)
       const uint32_t sid = ids_base + (uint32_t)slot * kMaxIds * 4;
       uint32_t off[kTile / RPP];
@@ -504,9 +525,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
         const int blk = lds_s32(sid + 4u * (uint32_t)min(max(jr - j0, 0), kMaxIds - 1));
         off[k] = ((uint32_t)blk * (uint32_t)c.b + (uint32_t)(t - jr * c.b)) * hD;
       }
+      if (!(c.debug & 256u)) {
 #pragma unroll
-      for (int k = 0; k < kTile / RPP; ++k)
-        if (t0 + RPP * k + rsub < T) cp_async16(dst0 + (uint32_t)(RPP * k * 128), lbase + off[k], 0);
+        for (int k = 0; k < kTile / RPP; ++k)
+          if (t0 + RPP * k + rsub < T) cp_async16(dst0 + (uint32_t)(RPP * k * 128), lbase + off[k], 0);
+      }
       cp_async_arrive_noinc(full0 + 8 * st);
       __syncwarp();
       if (lane == 0) mbar_arrive(ide0 + 8 * slot);
@@ -519,27 +542,40 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
       if (ld_unit >= units) break;
       if (g >= K::ST) {   // stage reuse: wait for the MMAs that read it
         const int st = g % K::ST;
-        mbar_wait(empty0 + 8 * st, ((g / K::ST) & 1) ^ 1);
+        mbar_wait_backoff(empty0 + 8 * st, ((g / K::ST) & 1) ^ 1, 100);
       }
       issue_next_load();
     }
 
   } else if (warp == 1) {
-    // ================= MMA issuer (single thread)
-    if (lane == 0) {
-      int kstep = 0, astep = 0;
-      for (int it = 0, unit = cluster_id; unit < units; ++it, unit += nclusters) {
-        const UnitInfo u = unit_info(unit);
-        const int qb = 0;
-        mbar_wait(qfull0, it & 1);
-        const uint32_t qbase = smem_u32(smem + K::OFF_Q0);
-        for (int i = 0; i < 2 * u.nt; ++i, ++kstep, ++astep) {
-          const int s = kstep % K::ST, a = astep & 1;
-          mbar_wait(acce0 + 8 * a, ((astep >> 1) & 1) ^ 1);
-          mbar_wait(full0 + 8 * s, (kstep / K::ST) & 1);
-          if ((c.debug & 1u) && blockIdx.x == 0 && kstep < 512)
-            reinterpret_cast<unsigned long long*>(c.ws.kept)[kstep * 4 + 1] = gtimer();
-          if (!(c.debug & 16u)) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // cp.async data -> tensor core
+    // ================= MMA issuer: lane 0 issues; the whole warp relays each step's completion to
+    // the epilogue through a hardware named barrier (bar.arrive), so the 256 epilogue threads block
+    // in bar.sync instead of polling the commit mbarrier (polls contended with MUFU in the MIO
+    // queue; measured). Step k-1 is relayed before step k is issued.
+    int kstep = 0, astep = 0;
+    auto relay = [&](int st) {          // wait MMA(st) complete, then release the epilogue for it
+      if (lane == 0) mbar_wait_backoff(accf0 + 8 * (st & 1), (st >> 1) & 1, 40);
+      __syncwarp();
+      if (!(c.debug & 4096u)) named_bar_arrive(2 + (st & 1), (kEpiWarps + 1) * 32);
+    };
+    for (int it = 0, unit = cluster_id; unit < units; ++it, unit += nclusters) {
+      const UnitInfo u = unit_info(unit);
+      const int qb = 0;
+      if (lane == 0) mbar_wait_backoff(qfull0, it & 1, 200);
+      __syncwarp();
+      const uint32_t qbase = smem_u32(smem + K::OFF_Q0);
+      for (int i = 0; i < 2 * u.nt; ++i, ++kstep, ++astep) {
+        if (astep > 0) relay(astep - 1);
+        const int s = kstep % K::ST, a = astep & 1;
+        if (lane == 0) {
+          const bool mrec = (c.debug & 1u) && blockIdx.x == 0 && astep < 1024;
+          unsigned long long* mdbg = reinterpret_cast<unsigned long long*>(c.ws.kept);
+          if (mrec) mdbg[16384 + astep * 4 + 0] = gtimer();
+          mbar_wait_backoff(acce0 + 8 * a, ((astep >> 1) & 1) ^ 1, 100);
+          if (mrec) mdbg[16384 + astep * 4 + 1] = gtimer();
+          if (!(c.debug & 2048u)) mbar_wait_backoff(full0 + 8 * s, (kstep / K::ST) & 1, 100);
+          if (mrec) mdbg[16384 + astep * 4 + 2] = gtimer();
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // cp.async data -> tensor core
           tc_fence_after();
           const uint32_t kb = smem_u32(Ks + s * K::STAGE_BYTES);
           const uint32_t dacc = tmem + a * 256;
@@ -562,14 +598,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
               umma(dacc, ad, bd, idesc_bf16(kTile, K::GW), k > 0);
             }
           }
+          if (mrec) mdbg[16384 + astep * 4 + 3] = gtimer();
           umma_commit(empty0 + 8 * s);   // K stage s free once these MMAs complete
-          if (c.debug & 8u) mbar_arrive(accf0 + 8 * a);
-          else umma_commit(accf0 + 8 * a);
+          umma_commit(accf0 + 8 * a);
         }
-        umma_commit(qempty0 + 8 * qb);     // Q buffer free once this unit's MMAs complete
+        __syncwarp();
       }
+      if (lane == 0) umma_commit(qempty0 + 8 * qb);     // Q buffer free once this unit's MMAs complete
+      __syncwarp();
     }
-    __syncwarp();
+    if (astep > 0) relay(astep - 1);
   } else if (warp >= kEpiWarp0) {
     // ================= epilogue warps (8): two per TMEM lane quarter
     const int ew = warp - kEpiWarp0;
@@ -627,7 +665,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
           continue;
         }
         const int a = astep & 1;
-        if (!(c.debug & 64u)) mbar_wait(accf0 + 8 * a, (astep >> 1) & 1);
+        const bool rec = (c.debug & 1u) && blockIdx.x == 0 && ew == 0 && lane == 0 && astep < 1024;
+        unsigned long long* dbg = reinterpret_cast<unsigned long long*>(c.ws.kept);
+        if (rec) dbg[8192 + astep * 4 + 0] = gtimer();
+        if (!(c.debug & 4096u)) named_bar(2 + a, (kEpiWarps + 1) * 32);   // MMA(astep) complete (relayed by warp 1)
+        if (rec) dbg[8192 + astep * 4 + 1] = gtimer();
         tc_fence_after();
         if ((c.debug & 1u) && blockIdx.x == 0 && ew == 0 && lane == 0 && astep < 512)
           reinterpret_cast<unsigned long long*>(c.ws.kept)[astep * 4 + 2] = gtimer();
@@ -638,21 +680,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
           if (lane == 0) mbar_arrive(acce0 + 8 * a);
         } else if (i < u.nt) {
           // ---- pass 1: this thread owns window column `col`; 128 token logits in TMEM, consumed
-          //      as 4 batches of 32 with the next batch's TMEM load in flight during the math
+          //      as 4 batches of 32 with the next batch's TMEM load in flight during the math. The
+          //      batch loop stays rolled (ping-pong pairs) so its body fits the L0 instruction cache.
           constexpr int NB = 32;
-          float vb[2][NB];
+          float va[NB], vb2[NB];
+          const uint32_t tbase_addr = lane_base + a * 256 + half * 128;
           if (warp_cols) {
-            TMEM_LD16(lane_base + a * 256 + half * 128, vb[0], 0);
-            TMEM_LD16(lane_base + a * 256 + half * 128 + 16, vb[0], 16);
+            TMEM_LD16(tbase_addr, va, 0);
+            TMEM_LD16(tbase_addr + 16, va, 16);
           }
-#pragma unroll
-          for (int bh = 0; bh < kTile / NB; ++bh) {
-            float* v = vb[bh & 1];
+          auto batch = [&](float* v, float* vnext, int bh) {
             if (warp_cols) tmem_wait_ld();
             if (bh + 1 < kTile / NB) {
               if (warp_cols) {
-                TMEM_LD16(lane_base + a * 256 + half * 128 + (bh + 1) * NB, vb[(bh + 1) & 1], 0);
-                TMEM_LD16(lane_base + a * 256 + half * 128 + (bh + 1) * NB + 16, vb[(bh + 1) & 1], 16);
+                TMEM_LD16(tbase_addr + (bh + 1) * NB, vnext, 0);
+                TMEM_LD16(tbase_addr + (bh + 1) * NB + 16, vnext, 16);
               }
             } else {
               tc_fence_before();
@@ -666,24 +708,24 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
                 for (int j = 0; j < NB; ++j)
                   if (tbase + j > limit1) v[j] = -INFINITY;
               }
-              // running reference m (no per-batch max): exact re-run only when the batch sum could
-              // overflow (first batch: m = -inf -> NaN/inf -> re-run)
-              float bsum = sum_exp_n<NB>(v, scale, m);
-              if (!(bsum < 1.8446744e19f)) {
-                float mx = v[0];
+              // online softmax normaliser: batch max first (3-input FMNMX, no branch on MUFU results,
+              // so the exp2 pipeline never drains at a batch boundary), then a branch-free rescale
+              float mx = max3f(v[0], v[1], v[2]);
 #pragma unroll
-                for (int j = 1; j < NB; j += 2) mx = (j + 1 < NB) ? max3f(mx, v[j], v[j + 1]) : fmaxf(mx, v[j]);
-                if (mx > -INFINITY) {
-                  const float mn = fmaxf(m, mx * scale);
-                  ssum = (m > -INFINITY) ? ssum * ex2f(m - mn) : 0.f;
-                  m = mn;
-                  bsum = sum_exp_n<NB>(v, scale, m);
-                } else {
-                  bsum = 0.f;
-                }
-              }
-              ssum += bsum;
+              for (int j = 3; j < NB - 1; j += 2) mx = max3f(mx, v[j], v[j + 1]);
+              mx = fmaxf(mx, v[NB - 1]);
+              const float mn = fmaxf(m, mx * scale);              // -inf only if nothing valid yet
+              const float mref = mn > -INFINITY ? mn : 0.f;
+              const float rescale = ex2f(m - mref);               // m = -inf -> 0 (ssum is 0 anyway)
+              const float bsum = sum_exp_n<NB>(v, scale, mref);
+              ssum = ssum * rescale + bsum;
+              m = mn;
             }
+          };
+#pragma unroll 1
+          for (int bh = 0; bh < kTile / NB; bh += 2) {
+            batch(va, vb2, bh);
+            batch(vb2, va, bh + 1);
           }
         } else {
           // ---- pass 2: this thread owns token t; the W/2 window rows of its half in batches of
@@ -734,6 +776,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
           if (half == 0 && t < u.T)
             c.ws.scores[(size_t)unit * c.max_seq_len + t] = (acc + cb[q * 32 + lane]) * (1.0f / W);
         }
+        if (rec) dbg[8192 + astep * 4 + 2] = gtimer();
         ++astep;
       }
     }

@@ -78,15 +78,40 @@ __device__ __forceinline__ float sum_exp_n(const float* v, float scale, float m)
   return a + b;
 }
 
-template <int WARPS, int NB>
-__global__ void __launch_bounds__(WARPS * 32, 1) k(float* out, int steps) {
+template <int WARPS, int NB, int LOADERS>
+__global__ void __launch_bounds__((WARPS + LOADERS) * 32, 1) k(float* out, int steps, const int4* gsrc, size_t gsz) {
   __shared__ uint32_t slot;
+  extern __shared__ __align__(1024) uint8_t ring[];
+  if (threadIdx.x == 0) *reinterpret_cast<volatile uint32_t*>(ring + 99 * 1024) = 0;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"((uint32_t)__cvta_generic_to_shared(&slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;"); __syncthreads(); asm volatile("tcgen05.fence::after_thread_sync;");
+  if (warp >= WARPS && LOADERS == 8) {   // idle warps: just wait for the end
+    volatile uint32_t* flag = reinterpret_cast<volatile uint32_t*>(ring + 99 * 1024);
+    while (*flag == 0) __nanosleep(1000);
+    asm volatile("tcgen05.fence::before_thread_sync;"); __syncthreads();
+    return;
+  }
+  if (warp >= WARPS) {   // loaders: stream 16-B cp.async (1 KB-strided rows) into a 96 KB smem ring until told to stop
+    const int lt = threadIdx.x - WARPS * 32;
+    size_t pos = ((size_t)blockIdx.x * 7919 + lt) * 64;
+    volatile uint32_t* flag = reinterpret_cast<volatile uint32_t*>(ring + 99 * 1024);
+    for (int it = 0; it < (1 << 30) && *flag == 0; ++it) {
+      for (int k = 0; k < 16; ++k) {
+        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(ring) + (uint32_t)(((it * 16 + k) * LOADERS * 32 + lt) % 6144) * 16;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(gsrc + (pos % gsz)) : "memory");
+        pos += 64 * 16 + 1;
+      }
+      asm volatile("cp.async.commit_group;");
+      asm volatile("cp.async.wait_group 2;");
+    }
+    asm volatile("cp.async.wait_all;");
+    asm volatile("tcgen05.fence::before_thread_sync;"); __syncthreads();
+    return;
+  }
   const int q = warp & 3, half = (warp >> 2) & 1;
   const uint32_t lane_base = slot + ((uint32_t)(q * 32) << 16) + half * 128 + ((warp >> 3) & 1) * 0;
   const float scale = 0.1275f;
@@ -110,15 +135,19 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k(float* out, int steps) {
     }
   }
   if (ssum == 1234.5f) out[0] = ssum;
+  if (threadIdx.x == 0) *reinterpret_cast<volatile uint32_t*>(ring + 99 * 1024) = 1;
   asm volatile("tcgen05.fence::before_thread_sync;"); __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(slot));
 }
-template <int WARPS, int NB>
+template <int WARPS, int NB, int LOADERS>
 void run() {
   float* out; cudaMalloc(&out, 4);
+  static int4* gsrc = nullptr; const size_t gsz = (size_t)1 << 28;
+  if (!gsrc) { cudaMalloc(&gsrc, gsz * 16); cudaMemset(gsrc, 0, gsz * 16); }
+  cudaFuncSetAttribute(k<WARPS, NB, LOADERS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
   const int steps = 3000; float ms = 0;
-  for (int r = 0; r < 2; ++r) { cudaEventRecord(a); k<WARPS, NB><<<148, WARPS * 32>>>(out, steps); cudaEventRecord(b); cudaEventSynchronize(b); cudaEventElapsedTime(&ms, a, b); }
-  printf("pass-1 step replica: %2d warps NB=%d: %.3f us/step (%s)\n", WARPS, NB, ms * 1e3 / steps, cudaGetErrorString(cudaGetLastError()));
+  for (int r = 0; r < 2; ++r) { cudaEventRecord(a); k<WARPS, NB, LOADERS><<<148, (WARPS + LOADERS) * 32, 100 * 1024>>>(out, steps, gsrc, gsz); cudaEventRecord(b); cudaEventSynchronize(b); cudaEventElapsedTime(&ms, a, b); }
+  printf("pass-1 step replica: %2d warps NB=%d loaders=%d: %.3f us/step (%s)\n", WARPS, NB, LOADERS, ms * 1e3 / steps, cudaGetErrorString(cudaGetLastError()));
 }
-int main() { run<8, 32>(); run<8, 16>(); return 0; }
+int main() { run<8, 32, 0>(); run<8, 32, 8>(); return 0; }
