@@ -154,6 +154,24 @@ def cpu_model():
     return "unknown"
 
 
+# ---------------------------------------------------------------- sharding (multi-GPU, weak scaling)
+def shard_rids(rank, world, per_gpu, R_total):
+    """Global request ids compressed by `rank`: a contiguous block of per_gpu ids (wrapping over
+    the config's R_total), so every rank's workload has the same shape (weak scaling) and data
+    are keyed by global request id (identical bytes whatever the GPU count)."""
+    return np.arange(rank * per_gpu, (rank + 1) * per_gpu) % R_total
+
+
+def max_over_ranks(value, dist=None, device=None):
+    """Job time = max over ranks (the contract's timing rule); NCCL on GPUs, gloo in CPU tests."""
+    if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
+        return float(value)
+    import torch
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 # ---------------------------------------------------------------- GPU arm
 def algorithmic_bytes(cfg, seq_lens, budgets, moves):
     """SURVEY §8(d) per-unit algorithmic bytes summed over the batch."""
@@ -227,7 +245,7 @@ def main():
     from paper_2603_08743_b200.batch import batch_of, desc_params
     from zpc_inputs.device import generate
 
-    rids = np.arange(rank * per_gpu, (rank + 1) * per_gpu) % cfg.R
+    rids = shard_rids(rank, world, per_gpu, cfg.R)
     w = generate(cfg, args.seed, rids, device=dev)
     flags = zipc.ZPC_F_COUNT_MOVES | (zipc.ZPC_F_SCORE_CUDACORE if args.cudacore else 0)
     desc, params = desc_params(w, flags=flags)
@@ -292,10 +310,7 @@ def main():
         for i in range(len(stages)):
             stage_ms[i] += evs[i].elapsed_time(evs[i + 1])
     step_ms_total = float(stage_ms.sum())
-    t = torch.tensor([step_ms_total], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    max_ms = float(t.item())
+    max_ms = max_over_ranks(step_ms_total, dist, dev)
     R_all = per_gpu * world
     ms_per_step = max_ms / args.steps
     value = R_all / (ms_per_step / 1000.0)
@@ -361,10 +376,8 @@ def main():
             assert int(host["status"][0]) == 0
             if i >= max(3, args.warmup):
                 e2e_ms += a.elapsed_time(b_)
-        te = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": R_all / (float(te.item()) / args.steps / 1e3), "unit": "req/s",
+        e2e_max = max_over_ranks(e2e_ms, dist, dev)
+        e2e = {"value": R_all / (e2e_max / args.steps / 1e3), "unit": "req/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "path": "zpc_compress_host: block tables, budgets, free stack, ref counts host-resident (pinned); "
                        "K/V/Q caches device-resident (the paged pool lives in HBM)"}
@@ -375,7 +388,8 @@ def main():
         cpu = {"value": v_cpu, "unit": "req/s", "cores": info["threads"], "kind": "oracle",
                "sample": info["sample"], "cpu": cpu_model(), "seconds": info["seconds"]}
 
-    launches_per_step = 2 + 2 + 1 + 1 + 2   # plan(2) score(lse+final) select compact finalize(2)
+    score_kernels = 2 if (args.cudacore or cfg.dtype != "bf16") else 1   # k_lse_cc+k_final_cc | k_score_tc
+    launches_per_step = 2 + score_kernels + 1 + 1 + 2   # plan(2) score select compact finalize(2)
     if rank == 0:
         line = {"metric": "requests_compressed_per_s", "value": value, "unit": "req/s", "n_gpus": world,
                 "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_per_step,

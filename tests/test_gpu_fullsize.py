@@ -1,0 +1,112 @@
+"""Full-size parity: BASELINE configs[1] (Qwen2.5-7B shape, 64 requests x 8192 tokens) in the
+launch configuration bench.py times, checked against the oracle on sampled units (inputs for the
+oracle are regenerated on the host by the numpy Philox generator, never read back from the GPU
+generator) plus size-independent invariants on every unit and request."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from paper_2603_08743_b200 import zipc
+from paper_2603_08743_b200.batch import batch_of, desc_params, workspace_view
+from zpc_inputs import CONFIGS, budgets_for, k_rows, q_rows, v_rows
+from zpc_inputs.device import generate
+
+from helpers import check_band, check_scores
+
+pytestmark = pytest.mark.gpu
+
+SAMPLES = [(0, 0, 0), (37, 13, 2), (63, 27, 3), (5, 21, 1)]
+
+
+@pytest.fixture(scope="module")
+def run7b():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    cfg = CONFIGS["qwen7b"]
+    rids = np.arange(cfg.R)
+    w = generate(cfg, 2603, rids)
+    tables0 = w.layout.tables.copy()
+    # pristine rows of the sampled units' target blocks are not needed: sources are regenerated
+    desc, params = desc_params(w, flags=zipc.ZPC_F_COUNT_MOVES)
+    b = batch_of(w, desc, params)
+    zipc.zpc_compress(desc, params, b)
+    torch.cuda.synchronize()
+    return cfg, w, desc, params, tables0
+
+
+def test_status_and_structure(run7b):
+    cfg, w, desc, params, tables0 = run7b
+    assert int(w.status.item()) == 0
+    R = cfg.R
+    T = 8192
+    N = T // cfg.b
+    nm = cfg.n_max
+    new_lens = w.new_lens.cpu().numpy()
+    np.testing.assert_array_equal(new_lens, np.minimum(T, w.budgets_host))
+    tables = w.tables.cpu().numpy()
+    # no prefix: in place: first N_max entries are the request's own first N_max blocks
+    np.testing.assert_array_equal(tables[:, :nm], tables0[:, :nm])
+    assert (w.new_num_blocks.cpu().numpy() == nm).all()
+    freed = w.freed.cpu().numpy()[:int(w.num_freed.item())]
+    expect = np.concatenate([tables0[r, nm:N] for r in range(R)])
+    np.testing.assert_array_equal(freed, expect)
+    top0 = w.layout.free_top
+    assert int(w.free_top.item()) == top0 + len(expect)
+    np.testing.assert_array_equal(w.free_stack.cpu().numpy()[top0:top0 + len(expect)], expect)
+
+
+def test_kept_lists_all_units(run7b):
+    """Every unit: kept list strictly ascending, length min(T, budget), window always kept."""
+    cfg, w, desc, params, _ = run7b
+    R = cfg.R
+    lay = zipc.zpc_workspace_layout_get(desc, params, R)
+    units = R * cfg.L * cfg.h_kv
+    kept = workspace_view(w, desc, params, "kept", torch.int32, (units, lay.kept_stride))
+    ell = w.new_lens.reshape(-1)
+    T = 8192
+    rng = torch.arange(lay.kept_stride, device=kept.device)
+    valid = rng[None, :] < ell[:, None]
+    k = torch.where(valid, kept, torch.full_like(kept, T))
+    assert bool(((k[:, 1:] > k[:, :-1]) | ~valid[:, 1:]).all())
+    assert bool(((k >= 0) & (k <= T)).all())
+    # window tokens T-w..T-1 are the last w kept entries of every unit
+    last = torch.gather(kept, 1, (ell[:, None] - cfg.w + torch.arange(cfg.w, device=kept.device)[None, :]).long())
+    assert bool((last == torch.arange(T - cfg.w, T, device=kept.device)[None, :]).all())
+
+
+@pytest.mark.parametrize("r,l,h", SAMPLES)
+def test_sampled_units_vs_oracle(run7b, r, l, h):
+    cfg, w, desc, params, tables0 = run7b
+    T = 8192
+    seed = 2603
+    # host regeneration of this unit's inputs (logical order), independent of the GPU generator
+    kt = k_rows(cfg, seed, r, l, h, np.arange(T), T)                 # bf16 bits [T, d]
+    q = q_rows(cfg, seed, r, l)                                       # [w, h_q, d]
+    geo = O.Geometry(L=1, h_kv=1, h_q=cfg.G, d=cfg.d, b=cfg.b, N_total=T // cfg.b, M=1, w=cfg.w, dtype="bf16")
+    kf = O.widen(kt, "bf16").reshape(T // cfg.b, cfg.b, 1, cfg.d)
+    qf = O.widen(q[:, h * cfg.G:(h + 1) * cfg.G, :], "bf16")
+    s_ref = O.attention_scores(O.logits_dense(geo, qf, kf, np.arange(T // cfg.b), T, 0), T)
+    R = cfg.R
+    units = R * cfg.L * cfg.h_kv
+    lay = zipc.zpc_workspace_layout_get(desc, params, R)
+    u = (r * cfg.L + l) * cfg.h_kv + h
+    S = workspace_view(w, desc, params, "scores", torch.float32, (units, w.max_seq_len))[u, :T].cpu().numpy()
+    check_scores(S, s_ref, f"unit {r},{l},{h}")
+    ell = int(w.new_lens[r, l, h].item())
+    kept = workspace_view(w, desc, params, "kept", torch.int32, (units, lay.kept_stride))[u, :ell].cpu().numpy()
+    check_band(kept, O.pin_window(O.max_pool(s_ref, cfg.pool_kernel), T, cfg.w), ell, f"unit {r},{l},{h}")
+    sel = O.select(O.pin_window(O.max_pool(S.astype(np.float64), cfg.pool_kernel), T, cfg.w), ell)
+    np.testing.assert_array_equal(sel, kept)
+    # bytes: rank i of the unit now holds the original row kept[i] (K and V), in the target blocks
+    vt = v_rows(cfg, seed, r, l, h, kept)
+    tbl = tables0[r]
+    ranks = np.arange(ell)
+    blk = torch.from_numpy(tbl[ranks // cfg.b].astype(np.int64)).to(w.k.device)
+    slot = torch.from_numpy((ranks % cfg.b).astype(np.int64)).to(w.k.device)
+    k_now = w.k[l][blk, slot, h].cpu().numpy().view(np.uint16)
+    v_now = w.v[l][blk, slot, h].cpu().numpy().view(np.uint16)
+    np.testing.assert_array_equal(k_now, kt[kept])
+    np.testing.assert_array_equal(v_now, vt)

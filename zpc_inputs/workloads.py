@@ -18,6 +18,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass, field
 
+import math
+
 import numpy as np
 
 from .philox import philox4x32
@@ -242,7 +244,9 @@ def make_layout(cfg: Config, seed, rids, table_stride=None) -> Layout:
         refs[tables[tables >= 0]] = 1
         refs[prefix] = R + 1          # every request + the harness's own reference
     M = R + 3
-    q_slots = ((np.arange(R) * 5 + 2) % M).astype(np.int32)
+    # distinct, non-identity slots: stride coprime to M (a permutation of the M slots)
+    stride_q = next(s for s in range(5, 5 + M + 1) if math.gcd(s, M) == 1)
+    q_slots = ((np.arange(R) * stride_q + 2) % M).astype(np.int32)
     return Layout(rids=rids, seq_lens=T, tables=tables, table_stride=stride, q_slots=q_slots, M=M,
                   N_total=N_total, free_stack=stack, free_top=len(free), ref_counts=refs,
                   prefix_blocks=prefix)
