@@ -24,6 +24,9 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include <cuda_bf16.h>
+#include <type_traits>
+
 #include "internal.h"
 
 namespace zpc {
@@ -38,6 +41,10 @@ constexpr int kIdSlots = 8;      // block-id ring (steps) filled by the walker, 
 constexpr int kIdGroup = 4;
 constexpr int kMaxIds = 32;      // block ids per 128-token tile (b >= 5)
 constexpr int kEpiWarps = 8;
+// setmaxnreg budget: 8 producer warps x kProdRegs + 8 epilogue warps x kEpiRegs <= 64K registers
+constexpr int kProdRegs = 72;
+constexpr int kEpiRegs = 184;
+static_assert(8 * kProdRegs + 8 * kEpiRegs <= 2048, "register file: 65536 = 32 lanes x 2048");
 constexpr uint32_t kL1Reserve = 0;   // L1 left unallocated (cp.async does not need it: measured)
 constexpr uint32_t kTmemCols = 512;
 constexpr float kLog2e = 1.4426950408889634f;
@@ -98,13 +105,14 @@ __device__ __forceinline__ int lds_s32(uint32_t addr) {
   asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
   return v;
 }
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, int /*unused*/) {
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
 // the mbarrier counts this thread's arrival once all its prior cp.async have landed
+// debug timeline stamp (ZPC_SCORE_DEBUG bit 1; CTA 0 only): SM cycle counter (%globaltimer ticks too coarsely)
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  asm volatile("mov.u64 %0, %clock64;" : "=l"(t));
   return t;
 }
 __device__ __forceinline__ void cp_async_arrive_noinc(uint32_t bar) {
@@ -150,6 +158,16 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   d |= (uint64_t)2 << 61;                      // SWIZZLE_128B
   return d;
 }
+// no-swizzle K-major descriptor (core matrices 8 rows x 16 B): LBO = K-direction core-matrix
+// stride, SBO = M/N-direction 8-row-group stride
+__device__ __forceinline__ uint64_t none_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;                      // descriptor version (sm_100); layout 0 = no swizzle
+  return d;
+}
 // Instruction descriptor, kind::f16: bf16 x bf16 -> fp32, both operands K-major.
 __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
@@ -158,6 +176,19 @@ __device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t a, uint64_t b, ui
   asm volatile(
       "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n"
       ::"r"(tmem_d), "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+// issued by one elected lane of a converged warp (operands warp-uniform -> uniform registers)
+__device__ __forceinline__ void umma_elect(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p, e;\n setp.ne.b32 p, %4, 0;\n elect.sync _|e, 0xffffffff;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n"
+      ::"r"(tmem_d), "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit_elect(uint32_t bar) {
+  asm volatile(
+      "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
+      " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(bar)
+      : "memory");
 }
 __device__ __forceinline__ void umma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
@@ -275,10 +306,19 @@ struct Cfg {
   // Shared memory and L1 are one 228 KB array on sm_100: the cp.async gather stages its in-flight
   // lines through L1, so the kernel leaves kL1Reserve bytes of it unallocated (DESIGN.md §Score
   // kernel, "L1 is the gather's in-flight buffer"). Q is therefore single-buffered.
-  static constexpr int STAGES_FIT = (int)((227 * 1024 - kL1Reserve - 1024 - MISC - Q_BYTES) / STAGE_BYTES);
+  // pass-2 normaliser folded into the MMA (a 9th K-step, no-swizzle K-major core matrices of
+  // 8 rows x 16 B; LBO = 128 B between the two K halves, SBO = 256 B between 8-row groups):
+  //   A_aug [kTile x 16] = ones in k = 0..2,  B_aug [GW x 16] = bf16 split (hi, mid, lo) of -L2/s
+  // so the pass-2 accumulator holds q.k - L2/s directly.
+  static constexpr uint32_t AUG_A_BYTES = kTile * 32;
+  static constexpr uint32_t AUG_B_BYTES = GW * 32;
+  static constexpr uint32_t OFF_AUG_A = Q_BYTES;
+  static constexpr uint32_t OFF_AUG_B = OFF_AUG_A + AUG_A_BYTES;
+  static constexpr uint32_t AUG_END = (OFF_AUG_B + AUG_B_BYTES + 1023) / 1024 * 1024;
+  static constexpr int STAGES_FIT = (int)((227 * 1024 - kL1Reserve - 1024 - MISC - AUG_END) / STAGE_BYTES);
   static constexpr int ST = STAGES_FIT > 6 ? 6 : STAGES_FIT;   // K ring depth
   static constexpr uint32_t OFF_Q0 = 0;
-  static constexpr uint32_t OFF_K = Q_BYTES;
+  static constexpr uint32_t OFF_K = AUG_END;
   static constexpr uint32_t OFF_F = OFF_K + ST * STAGE_BYTES;        // floats
   static constexpr uint32_t OFF_IDS = OFF_F + (2 * 256 * 2 + 256 + 2 * kTile) * 4;
   static constexpr uint32_t OFF_BAR = OFF_IDS + kIdSlots * kMaxIds * 4;
@@ -358,6 +398,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
   const uint32_t accf0 = smem_u32(bars + 8), acce0 = smem_u32(bars + 10);
   const uint32_t qfull0 = smem_u32(bars + 12), qempty0 = smem_u32(bars + 14);
   const uint32_t xchg0 = smem_u32(bars + 16);
+  const uint32_t augf = smem_u32(bars + 18);                  // B_aug of the current unit written
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rank = C > 1 ? (int)(blockIdx.x % C) : 0;
@@ -375,10 +416,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
       mbar_init(xchg0 + 8 * a, C);
     }
     for (int k = 0; k < kIdSlots; ++k) { mbar_init(idf0 + 8 * k, 1); mbar_init(ide0 + 8 * k, kLoadWarps); }
+    mbar_init(augf, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_q)));
+  }
+  {
+    // A_aug rows: bf16 1.0 in k = 0..2, zeros elsewhere; B_aug starts all zero (k = 3..15 stay 0)
+    uint4* aug = reinterpret_cast<uint4*>(smem + K::OFF_AUG_A);
+    for (int i = threadIdx.x; i < (int)((K::AUG_A_BYTES + K::AUG_B_BYTES) / 16); i += kThreads) {
+      uint4 v = make_uint4(0u, 0u, 0u, 0u);
+      // 16-B chunk i of A_aug: (group, khalf, row%8) = (i / 16, (i / 8) & 1, i % 8); khalf 0 holds k 0..7
+      if (i < (int)(K::AUG_A_BYTES / 16) && ((i >> 3) & 1) == 0) v = make_uint4(0x3F803F80u, 0x00003F80u, 0u, 0u);
+      aug[i] = v;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -410,6 +463,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
   // streamed tiles are the ones most likely still in L2)
   auto tile_of = [](const UnitInfo& u, int i) { return i < u.nt ? u.tb + i : u.tb + (2 * u.nt - 1 - i); };
 
+  // register rebalance per warpgroup (setmaxnreg must dominate each role's code so ptxas
+  // allocates the epilogue with kEpiRegs): the producers need few registers, the epilogue's latency
+  // hiding (batches in flight, hoisted TMEM loads) needs many
+  if (warp < kEpiWarp0) {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kProdRegs));
   if (warp == 0) {
     // ================= Q producer: one TMA box per 64-element slab per unit (double buffer)
     if (lane == 0) {
@@ -528,7 +586,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
       if (!(c.debug & 256u)) {
 #pragma unroll
         for (int k = 0; k < kTile / RPP; ++k)
-          if (t0 + RPP * k + rsub < T) cp_async16(dst0 + (uint32_t)(RPP * k * 128), lbase + off[k], 0);
+          if (t0 + RPP * k + rsub < T) cp_async16(dst0 + (uint32_t)(RPP * k * 128), lbase + off[k]);
       }
       cp_async_arrive_noinc(full0 + 8 * st);
       __syncwarp();
@@ -547,68 +605,74 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
       issue_next_load();
     }
 
+  } else if (warp == 3) {
+    // ================= relay: each step's MMA completion (commit mbarrier) is passed to the
+    // epilogue through a hardware named barrier (bar.arrive), so the 256 epilogue threads block in
+    // bar.sync instead of polling; kept off the MMA warp so MMA(k) issues without waiting for
+    // MMA(k-1) to finish (back-to-back on the tensor pipe; measured: pass 2 was MMA-serialised).
+    // Barrier reuse is safe: MMA(k+2) needs acc_empty(k), i.e. every epilogue warp past barrier k.
+    int astep = 0;
+    for (int unit = cluster_id; unit < units; unit += nclusters) {
+      const UnitInfo u = unit_info(unit);
+      for (int i = 0; i < 2 * u.nt; ++i, ++astep) {
+        if (lane == 0) mbar_wait(accf0 + 8 * (astep & 1), (astep >> 1) & 1);
+        __syncwarp();
+        named_bar_arrive(2 + (astep & 1), (kEpiWarps + 1) * 32);
+      }
+    }
   } else if (warp == 1) {
-    // ================= MMA issuer: lane 0 issues; the whole warp relays each step's completion to
-    // the epilogue through a hardware named barrier (bar.arrive), so the 256 epilogue threads block
-    // in bar.sync instead of polling the commit mbarrier (polls contended with MUFU in the MIO
-    // queue; measured). Step k-1 is relayed before step k is issued.
+    // ================= MMA issuer: the whole warp runs converged (descriptors are warp-uniform,
+    // so ptxas keeps them in uniform registers) and one elected lane issues each tcgen05.mma /
+    // commit; a lane-0-only region made ptxas wrap every MMA in an ELECT/R2UR/BRA.U.ANY loop
+    // (~100 cycles per issue, measured: the 9-MMA pass-2 step could not keep the tensor pipe fed).
+    // Completion is relayed to the epilogue by warp 3.
     int kstep = 0, astep = 0;
-    auto relay = [&](int st) {          // wait MMA(st) complete, then release the epilogue for it
-      if (lane == 0) mbar_wait_backoff(accf0 + 8 * (st & 1), (st >> 1) & 1, 40);
-      __syncwarp();
-      if (!(c.debug & 4096u)) named_bar_arrive(2 + (st & 1), (kEpiWarps + 1) * 32);
-    };
+    const uint64_t aug_a = none_desc(smem_u32(smem + K::OFF_AUG_A), 128, 256);
+    const uint64_t aug_b = none_desc(smem_u32(smem + K::OFF_AUG_B), 128, 256);
+    const uint64_t qd0 = sw128_desc(smem_u32(smem + K::OFF_Q0));
     for (int it = 0, unit = cluster_id; unit < units; ++it, unit += nclusters) {
       const UnitInfo u = unit_info(unit);
-      const int qb = 0;
-      if (lane == 0) mbar_wait_backoff(qfull0, it & 1, 200);
-      __syncwarp();
-      const uint32_t qbase = smem_u32(smem + K::OFF_Q0);
+      mbar_wait(qfull0, it & 1);
       for (int i = 0; i < 2 * u.nt; ++i, ++kstep, ++astep) {
-        if (astep > 0) relay(astep - 1);
         const int s = kstep % K::ST, a = astep & 1;
-        if (lane == 0) {
-          const bool mrec = (c.debug & 1u) && blockIdx.x == 0 && astep < 1024;
-          unsigned long long* mdbg = reinterpret_cast<unsigned long long*>(c.ws.kept);
-          if (mrec) mdbg[16384 + astep * 4 + 0] = gtimer();
-          mbar_wait_backoff(acce0 + 8 * a, ((astep >> 1) & 1) ^ 1, 100);
-          if (mrec) mdbg[16384 + astep * 4 + 1] = gtimer();
-          if (!(c.debug & 2048u)) mbar_wait_backoff(full0 + 8 * s, (kstep / K::ST) & 1, 100);
-          if (mrec) mdbg[16384 + astep * 4 + 2] = gtimer();
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // cp.async data -> tensor core
-          tc_fence_after();
-          const uint32_t kb = smem_u32(Ks + s * K::STAGE_BYTES);
-          const uint32_t dacc = tmem + a * 256;
-          if (c.debug & 4u) {
-            // debug: no MMA
-          } else if (i < u.nt) {
+        const bool mrec = (c.debug & 1u) && blockIdx.x == 0 && astep < 1024 && lane == 0;
+        unsigned long long* mdbg = reinterpret_cast<unsigned long long*>(c.ws.kept);
+        if (mrec) mdbg[16384 + astep * 4 + 0] = gtimer();
+        mbar_wait(acce0 + 8 * a, ((astep >> 1) & 1) ^ 1);
+        if (mrec) mdbg[16384 + astep * 4 + 1] = gtimer();
+        if (!(c.debug & 2048u)) mbar_wait(full0 + 8 * s, (kstep / K::ST) & 1);
+        if (i == u.nt) mbar_wait(augf, it & 1);   // this unit's -L2/s is in B_aug
+        if (mrec) mdbg[16384 + astep * 4 + 2] = gtimer();
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // cp.async data -> tensor core
+        tc_fence_after();
+        const uint64_t kd0 = sw128_desc(smem_u32(Ks + s * K::STAGE_BYTES));
+        const uint32_t dacc = tmem + a * 256;
+        // descriptor start addresses are in 16-B units: a byte offset o adds o >> 4
+        if (c.debug & 4u) {
+          // debug: no MMA
+        } else if (i < u.nt) {
 #pragma unroll
-            for (int half = 0; half < K::M1H; ++half)
+          for (int half = 0; half < K::M1H; ++half)
 #pragma unroll
-              for (int k = 0; k < K::KSTEPS; ++k) {
-                const uint64_t ad = sw128_desc(qbase + (k >> 2) * K::SLAB_Q + half * 128 * 128 + (k & 3) * 32);
-                const uint64_t bd = sw128_desc(kb + (k >> 2) * K::SLAB_K + (k & 3) * 32);
-                umma(dacc + half * 128, ad, bd, idesc_bf16(128, kTile), k > 0);
-              }
-          } else {
+            for (int k = 0; k < K::KSTEPS; ++k)
+              umma_elect(dacc + half * 128, qd0 + (((k >> 2) * K::SLAB_Q + half * 128 * 128 + (k & 3) * 32) >> 4),
+                         kd0 + (((k >> 2) * K::SLAB_K + (k & 3) * 32) >> 4), idesc_bf16(128, kTile), k > 0);
+        } else {
 #pragma unroll
-            for (int k = 0; k < K::KSTEPS; ++k) {
-              const uint64_t ad = sw128_desc(kb + (k >> 2) * K::SLAB_K + (k & 3) * 32);
-              const uint64_t bd = sw128_desc(qbase + (k >> 2) * K::SLAB_Q + (k & 3) * 32);
-              umma(dacc, ad, bd, idesc_bf16(kTile, K::GW), k > 0);
-            }
-          }
-          if (mrec) mdbg[16384 + astep * 4 + 3] = gtimer();
-          umma_commit(empty0 + 8 * s);   // K stage s free once these MMAs complete
-          umma_commit(accf0 + 8 * a);
+          for (int k = 0; k < K::KSTEPS; ++k)
+            umma_elect(dacc, kd0 + (((k >> 2) * K::SLAB_K + (k & 3) * 32) >> 4),
+                       qd0 + (((k >> 2) * K::SLAB_Q + (k & 3) * 32) >> 4), idesc_bf16(kTile, K::GW), k > 0);
+          umma_elect(dacc, aug_a, aug_b, idesc_bf16(kTile, K::GW), 1);
         }
-        __syncwarp();
+        if (mrec) mdbg[16384 + astep * 4 + 3] = gtimer();
+        umma_commit_elect(empty0 + 8 * s);   // K stage s free once these MMAs complete
+        umma_commit_elect(accf0 + 8 * a);
       }
-      if (lane == 0) umma_commit(qempty0 + 8 * qb);     // Q buffer free once this unit's MMAs complete
-      __syncwarp();
+      umma_commit_elect(qempty0);            // Q buffer free once this unit's MMAs complete
     }
-    if (astep > 0) relay(astep - 1);
-  } else if (warp >= kEpiWarp0) {
+  }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kEpiRegs));
     // ================= epilogue warps (8): two per TMEM lane quarter
     const int ew = warp - kEpiWarp0;
     const int q = warp & 3;
@@ -619,7 +683,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
     const int u1 = col_ok ? col / G : 0;
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
 
+    // B_aug row of column c: (hi, mid, lo) bf16 with hi + mid + lo = -L2/s to ~2^-24 relative
+    auto write_aug = [&](int cc, float L2) {
+      const float nv = -L2 / scale;
+      const __nv_bfloat16 hi = __float2bfloat16_rn(nv);
+      const float r1 = nv - __bfloat162float(hi);
+      const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
+      const __nv_bfloat16 lo = __float2bfloat16_rn(r1 - __bfloat162float(mid));
+      const uint32_t w0 = (uint32_t)__bfloat16_as_ushort(hi) | ((uint32_t)__bfloat16_as_ushort(mid) << 16);
+      const uint32_t w1 = (uint32_t)__bfloat16_as_ushort(lo);
+      *reinterpret_cast<uint2*>(smem + K::OFF_AUG_B + (cc >> 3) * 256 + (cc & 7) * 16) = make_uint2(w0, w1);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // visible to the tensor core
+    };
     int astep = 0;
+    // debug timing (bit 1): [0] P1 step work, [2] P1 gap before step, [3] P2 ld, [4] P2 math, [5] P2 gap,
+    // [1] P1 steps, [6] P2 work (start..end), [7] P2 steps
+    unsigned long long tacc[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tlast = gtimer();
     for (int it = 0, unit = cluster_id; unit < units; ++it, unit += nclusters) {
       const UnitInfo u = unit_info(unit);
       const int limit1 = u.T - W + u1;   // pass-1 causal limit of this column (R1, R2)
@@ -631,7 +710,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
           if (C == 1) {
             if (col_ok) {
               const float L2 = m + lg2f(ssum);
-              negL[col] = -L2;
+              write_aug(col, L2);
               c.ws.lse[(size_t)unit * K::GW + col] = L2;
             }
           } else {
@@ -656,11 +735,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
               for (int rr = 0; rr < C; ++rr)
                 if (mr[rr] > -INFINITY) S += sr[rr] * ex2f(mr[rr] - M);
               const float L2 = M + lg2f(S);
-              negL[col] = -L2;
+              write_aug(col, L2);
               if (rank == 0) c.ws.lse[(size_t)unit * K::GW + col] = L2;
             }
           }
           named_bar(1, kEpiWarps * 32);
+          if (ew == 0 && lane == 0) mbar_arrive(augf);   // pass-2 MMAs of this unit may start
           if (i == 2 * u.nt) break;
           continue;
         }
@@ -668,8 +748,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
         const bool rec = (c.debug & 1u) && blockIdx.x == 0 && ew == 0 && lane == 0 && astep < 1024;
         unsigned long long* dbg = reinterpret_cast<unsigned long long*>(c.ws.kept);
         if (rec) dbg[8192 + astep * 4 + 0] = gtimer();
-        if (!(c.debug & 4096u)) named_bar(2 + a, (kEpiWarps + 1) * 32);   // MMA(astep) complete (relayed by warp 1)
+        named_bar(2 + a, (kEpiWarps + 1) * 32);   // MMA(astep) complete (relayed by warp 3)
         if (rec) dbg[8192 + astep * 4 + 1] = gtimer();
+        const unsigned long long ts0 = (c.debug & 1u) ? gtimer() : 0ull;   // per-warp register timing
+        if (c.debug & 1u) { tacc[(i < u.nt ? 0 : 3) + 2] += ts0 - tlast; }
         tc_fence_after();
         if ((c.debug & 1u) && blockIdx.x == 0 && ew == 0 && lane == 0 && astep < 512)
           reinterpret_cast<unsigned long long*>(c.ws.kept)[astep * 4 + 2] = gtimer();
@@ -685,100 +767,112 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
           constexpr int NB = 32;
           float va[NB], vb2[NB];
           const uint32_t tbase_addr = lane_base + a * 256 + half * 128;
+          // warp-uniform: G*w = 32*G, so a warp's 32 columns are all valid or all padding
           if (warp_cols) {
             TMEM_LD16(tbase_addr, va, 0);
             TMEM_LD16(tbase_addr + 16, va, 16);
           }
-          auto batch = [&](float* v, float* vnext, int bh) {
-            if (warp_cols) tmem_wait_ld();
+          // the causal limit only bites in the last tile(s) of a unit: a warp-uniform test per step
+          // selects the masking variant, so the hot variant has no per-element compare or branch
+          const bool need_mask = t0 + kTile - 1 > u.T - W;
+          auto batch = [&](float* v, float* vnext, int bh, auto mask_tag) {
+            constexpr bool kMask = decltype(mask_tag)::value;
+            tmem_wait_ld();
             if (bh + 1 < kTile / NB) {
-              if (warp_cols) {
-                TMEM_LD16(tbase_addr + (bh + 1) * NB, vnext, 0);
-                TMEM_LD16(tbase_addr + (bh + 1) * NB + 16, vnext, 16);
-              }
+              TMEM_LD16(tbase_addr + (bh + 1) * NB, vnext, 0);
+              TMEM_LD16(tbase_addr + (bh + 1) * NB + 16, vnext, 16);
             } else {
               tc_fence_before();
               __syncwarp();
               if (lane == 0) mbar_arrive(acce0 + 8 * a);
             }
-            if (col_ok) {
+            if constexpr (kMask) {
               const int tbase = t0 + bh * NB;
-              if (tbase + NB - 1 > limit1) {
 #pragma unroll
-                for (int j = 0; j < NB; ++j)
-                  if (tbase + j > limit1) v[j] = -INFINITY;
-              }
-              // online softmax normaliser: batch max first (3-input FMNMX, no branch on MUFU results,
-              // so the exp2 pipeline never drains at a batch boundary), then a branch-free rescale
-              float mx = max3f(v[0], v[1], v[2]);
-#pragma unroll
-              for (int j = 3; j < NB - 1; j += 2) mx = max3f(mx, v[j], v[j + 1]);
-              mx = fmaxf(mx, v[NB - 1]);
-              const float mn = fmaxf(m, mx * scale);              // -inf only if nothing valid yet
-              const float mref = mn > -INFINITY ? mn : 0.f;
-              const float rescale = ex2f(m - mref);               // m = -inf -> 0 (ssum is 0 anyway)
-              const float bsum = sum_exp_n<NB>(v, scale, mref);
-              ssum = ssum * rescale + bsum;
-              m = mn;
+              for (int j = 0; j < NB; ++j) v[j] = (tbase + j > limit1) ? -INFINITY : v[j];
             }
+            // online softmax normaliser: batch max (3-input FMNMX), branch-free rescale
+            float mx = max3f(v[0], v[1], v[2]);
+#pragma unroll
+            for (int j = 3; j < NB - 1; j += 2) mx = max3f(mx, v[j], v[j + 1]);
+            mx = fmaxf(mx, v[NB - 1]);
+            const float mn = fmaxf(m, mx * scale);              // -inf only if nothing valid yet
+            const float mref = mn > -INFINITY ? mn : 0.f;
+            const float rescale = ex2f(m - mref);               // m = -inf -> 0 (ssum is 0 anyway)
+            const float bsum = sum_exp_n<NB>(v, scale, mref);
+            ssum = ssum * rescale + bsum;
+            m = mn;
           };
+          if (!warp_cols) {
+            // padding warp (columns >= G*w): only the accumulator release
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(acce0 + 8 * a);
+          } else if (!need_mask) {
 #pragma unroll 1
-          for (int bh = 0; bh < kTile / NB; bh += 2) {
-            batch(va, vb2, bh);
-            batch(vb2, va, bh + 1);
+            for (int bh = 0; bh < kTile / NB; bh += 2) {
+              batch(va, vb2, bh, std::false_type{});
+              batch(vb2, va, bh + 1, std::false_type{});
+            }
+          } else {
+#pragma unroll 1
+            for (int bh = 0; bh < kTile / NB; bh += 2) {
+              batch(va, vb2, bh, std::true_type{});
+              batch(vb2, va, bh + 1, std::true_type{});
+            }
           }
         } else {
-          // ---- pass 2: this thread owns token t; the W/2 window rows of its half in batches of
-          //      UB rows (UB*G columns, loaded from TMEM in 16-column chunks, LSE as float4)
+          // ---- pass 2: this thread owns token t and the W/2 window rows of its half. The MMA
+          //      already subtracted L2/s (B_aug), so each row is max over its G heads, one FMUL,
+          //      one exp2: S[t] = (1/w) sum_u 2^(s * max_g (q_ug.k_t - L2_ug/s))  (Alg. 2 / Eq. 3)
           const int t = t0 + q * 32 + lane;
           const int du = t - (u.T - W) - half * (W / 2);   // row uu of this half is causal iff uu >= du
-          float acc0 = 0.f, acc1 = 0.f;
+          float v[K::HC];
 #pragma unroll
-          for (int bb = 0; bb < (W / 2) / K::UB; ++bb) {
-            constexpr int BC = K::UB * G;                   // columns per batch
-            const int c0 = bb * BC;                         // first column of the batch (in half)
-            const int l0 = (c0 / 16) * 16;                  // 16-aligned TMEM load window
-            const int nld = (c0 + BC - l0 + 15) / 16;
-            float v[K::LDMAX * 16];
+          for (int k = 0; k < K::HC / 16; ++k) TMEM_LD16(lane_base + a * 256 + half * K::HC + k * 16, v, k * 16);
+          tmem_wait_ld();
+          const unsigned long long ts1 = (c.debug & 1u) ? gtimer() : 0ull;
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(acce0 + 8 * a);       // accumulator free for MMA(astep + 2)
+          float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-            for (int k = 0; k < K::LDMAX; ++k)
-              if (k < nld) TMEM_LD16(lane_base + a * 256 + half * K::HC + l0 + k * 16, v, k * 16);
-            float Lv[BC];
-            const uint32_t L4 = smem_u32(negL + half * K::HC + c0);
+          for (int uu = 0; uu < W / 2; ++uu) {
+            const float* y = v + uu * G;
+            float mx;
+            if constexpr (G == 4) mx = fmaxf(max3f(y[0], y[1], y[2]), y[3]);
+            else if constexpr (G == 5) mx = max3f(max3f(y[0], y[1], y[2]), y[3], y[4]);
+            else if constexpr (G == 7) mx = max3f(max3f(y[0], y[1], y[2]), max3f(y[3], y[4], y[5]), y[6]);
+            else if constexpr (G == 8) mx = max3f(max3f(y[0], y[1], y[2]), max3f(y[3], y[4], y[5]), fmaxf(y[6], y[7]));
+            else {
+              mx = y[0];
 #pragma unroll
-            for (int j = 0; j < BC / 4; ++j)
-              asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                           : "=f"(Lv[4 * j]), "=f"(Lv[4 * j + 1]), "=f"(Lv[4 * j + 2]), "=f"(Lv[4 * j + 3])
-                           : "r"(L4 + 16u * j));
-            tmem_wait_ld();
-            if (bb == (W / 2) / K::UB - 1) {
-              tc_fence_before();
-              __syncwarp();
-              if (lane == 0) mbar_arrive(acce0 + 8 * a);
+              for (int g = 1; g < G; ++g) mx = fmaxf(mx, y[g]);
             }
-#pragma unroll
-            for (int uu = 0; uu < K::UB; ++uu) {
-              const int o = c0 - l0 + uu * G;
-              float mx = fmaf(v[o], scale, Lv[uu * G]);
-#pragma unroll
-              for (int g = 1; g < G; g += 2)
-                mx = (g + 1 < G) ? max3f(mx, fmaf(v[o + g], scale, Lv[uu * G + g]),
-                                         fmaf(v[o + g + 1], scale, Lv[uu * G + g + 1]))
-                                 : fmaxf(mx, fmaf(v[o + g], scale, Lv[uu * G + g]));
-              const float pterm = (bb * K::UB + uu >= du) ? ex2f(mx) : 0.f;
-              if (uu & 1) acc1 += pterm; else acc0 += pterm;
-            }
+            const float pterm = ex2f(mx * scale);
+            acc[uu & 3] += (uu >= du) ? pterm : 0.f;
           }
-          const float acc = acc0 + acc1;
+          const float accs = (acc[0] + acc[1]) + (acc[2] + acc[3]);
           float* cb = comb + (astep & 1) * kTile;
-          if (half == 1) cb[q * 32 + lane] = acc;
+          if (half == 1) cb[q * 32 + lane] = accs;
+          if (c.debug & 1u) { const unsigned long long ts2 = gtimer(); tacc[3] += ts1 - ts0; tacc[4] += ts2 - ts1; }
           named_bar(1, kEpiWarps * 32);
-          if (half == 0 && t < u.T)
-            c.ws.scores[(size_t)unit * c.max_seq_len + t] = (acc + cb[q * 32 + lane]) * (1.0f / W);
+          if (half == 0 && t < u.T && !(c.debug & 16384u))
+            c.ws.scores[(size_t)unit * c.max_seq_len + t] = (accs + cb[q * 32 + lane]) * (1.0f / W);
         }
         if (rec) dbg[8192 + astep * 4 + 2] = gtimer();
+        if (c.debug & 1u) {
+          const unsigned long long te = gtimer();
+          if (i < u.nt) { tacc[0] += te - ts0; tacc[1] += 1; } else { tacc[6] += te - ts0; tacc[7] += 1; }
+          tlast = te;
+        }
         ++astep;
       }
+    }
+    if ((c.debug & 1u) && lane == 0) {   // per-warp, per-CTA totals (cycles) -> kept[65536 + (cta*8 + ew)*8 + k]
+      unsigned long long* out = reinterpret_cast<unsigned long long*>(c.ws.kept) + 65536 + ((size_t)blockIdx.x * 8 + ew) * 8;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) out[k] = tacc[k];
     }
   }
   // ---- teardown
