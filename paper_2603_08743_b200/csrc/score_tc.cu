@@ -615,9 +615,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
     for (int unit = cluster_id; unit < units; unit += nclusters) {
       const UnitInfo u = unit_info(unit);
       for (int i = 0; i < 2 * u.nt; ++i, ++astep) {
+        const bool rrec = (c.debug & 1u) && blockIdx.x == 0 && lane == 0 && astep < 1024;
+        unsigned long long* rdbg = reinterpret_cast<unsigned long long*>(c.ws.kept) + 40960;
+        if (rrec) rdbg[astep * 2 + 0] = gtimer();
         if (lane == 0) mbar_wait(accf0 + 8 * (astep & 1), (astep >> 1) & 1);
         __syncwarp();
-        named_bar_arrive(2 + (astep & 1), (kEpiWarps + 1) * 32);
+        if (rrec) rdbg[astep * 2 + 1] = gtimer();
+        if (c.debug & 8u) named_bar_arrive(2 + (astep & 1), (kEpiWarps + 1) * 32);
       }
     }
   } else if (warp == 1) {
@@ -698,14 +702,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
     int astep = 0;
     // debug timing (bit 1): [0] P1 step work, [2] P1 gap before step, [3] P2 ld, [4] P2 math, [5] P2 gap,
     // [1] P1 steps, [6] P2 work (start..end), [7] P2 steps
-    unsigned long long tacc[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tlast = gtimer();
+    uint32_t tacc[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tlast = (uint32_t)gtimer();
     for (int it = 0, unit = cluster_id; unit < units; ++it, unit += nclusters) {
       const UnitInfo u = unit_info(unit);
       const int limit1 = u.T - W + u1;   // pass-1 causal limit of this column (R1, R2)
-      float m = -INFINITY, ssum = 0.f;
+      float m = -INFINITY, ssum = 0.f, m1 = -INFINITY, s1 = 0.f;   // two pass-1 streams (see pair())
       for (int i = 0; i <= 2 * u.nt; ++i) {
         if (i == u.nt) {
           // ---- end of pass 1: LSE per column, combined across the cluster through DSMEM
+          {   // merge the two streams into (m, ssum)
+            const float mm = fmaxf(m, m1);
+            const float mr = mm > -INFINITY ? mm : 0.f;
+            ssum = ssum * ex2f(m - mr) + s1 * ex2f(m1 - mr);
+            m = mm;
+          }
           const int pb = it & 1;
           if (C == 1) {
             if (col_ok) {
@@ -748,9 +758,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
         const bool rec = (c.debug & 1u) && blockIdx.x == 0 && ew == 0 && lane == 0 && astep < 1024;
         unsigned long long* dbg = reinterpret_cast<unsigned long long*>(c.ws.kept);
         if (rec) dbg[8192 + astep * 4 + 0] = gtimer();
-        named_bar(2 + a, (kEpiWarps + 1) * 32);   // MMA(astep) complete (relayed by warp 3)
+        // MMA(astep) complete: each warp waits the commit mbarrier itself (try_wait parks the warp;
+        // no cross-warp barrier, so warps are not held to the slowest one every step). No phase
+        // aliasing: MMA(astep + 2) needs every epilogue warp's acc_empty arrival for astep.
+        if (c.debug & 8u) named_bar(2 + a, (kEpiWarps + 1) * 32);   // bisection: relay-warp barrier
+        else mbar_wait(accf0 + 8 * a, (astep >> 1) & 1);
         if (rec) dbg[8192 + astep * 4 + 1] = gtimer();
-        const unsigned long long ts0 = (c.debug & 1u) ? gtimer() : 0ull;   // per-warp register timing
+        const uint32_t ts0 = (c.debug & 1u) ? (uint32_t)gtimer() : 0u;   // per-warp register timing (mod 2^32)
         if (c.debug & 1u) { tacc[(i < u.nt ? 0 : 3) + 2] += ts0 - tlast; }
         tc_fence_after();
         if ((c.debug & 1u) && blockIdx.x == 0 && ew == 0 && lane == 0 && astep < 512)
@@ -764,45 +778,53 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
           // ---- pass 1: this thread owns window column `col`; 128 token logits in TMEM, consumed
           //      as 4 batches of 32 with the next batch's TMEM load in flight during the math. The
           //      batch loop stays rolled (ping-pong pairs) so its body fits the L0 instruction cache.
+          // Two independent online (max, sum) streams per column -- even 32-token batches into
+          // (m0, s0), odd ones into (m1, s1), merged at the end of pass 1 -- so each 64-token pair
+          // carries two exp2 chains with no dependence between them (the MUFU pipe is fed from
+          // both); the next pair's TMEM load is in flight during the math.
           constexpr int NB = 32;
-          float va[NB], vb2[NB];
+          float vp[2 * NB];
           const uint32_t tbase_addr = lane_base + a * 256 + half * 128;
-          // warp-uniform: G*w = 32*G, so a warp's 32 columns are all valid or all padding
-          if (warp_cols) {
-            TMEM_LD16(tbase_addr, va, 0);
-            TMEM_LD16(tbase_addr + 16, va, 16);
-          }
           // the causal limit only bites in the last tile(s) of a unit: a warp-uniform test per step
           // selects the masking variant, so the hot variant has no per-element compare or branch
           const bool need_mask = t0 + kTile - 1 > u.T - W;
-          auto batch = [&](float* v, float* vnext, int bh, auto mask_tag) {
+          auto online = [&](const float* v, float& mm, float& ss) {
+            // batch max as a depth-4 tree of 3-input FMNMX (a linear chain is 16 deep)
+            float t3[11];
+#pragma unroll
+            for (int j = 0; j < 10; ++j) t3[j] = max3f(v[3 * j], v[3 * j + 1], v[3 * j + 2]);
+            t3[10] = fmaxf(v[30], v[31]);
+            const float mx = fmaxf(max3f(max3f(t3[0], t3[1], t3[2]), max3f(t3[3], t3[4], t3[5]),
+                                         max3f(t3[6], t3[7], t3[8])),
+                                   fmaxf(t3[9], t3[10]));
+            const float mn = fmaxf(mm, mx * scale);             // -inf only if nothing valid yet
+            const float mref = mn > -INFINITY ? mn : 0.f;
+            const float rescale = ex2f(mm - mref);              // mm = -inf -> 0 (ss is 0 anyway)
+            const float bsum = sum_exp_n<NB>(v, scale, mref);
+            ss = ss * rescale + bsum;
+            mm = mn;
+          };
+          // one 64-token pair: load, wait, two independent exp2 chains (the second warp of the SMSP
+          // covers the load latency)
+          auto pair = [&](int bp, auto mask_tag) {
             constexpr bool kMask = decltype(mask_tag)::value;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) TMEM_LD16(tbase_addr + bp * 2 * NB + k * 16, vp, k * 16);
             tmem_wait_ld();
-            if (bh + 1 < kTile / NB) {
-              TMEM_LD16(tbase_addr + (bh + 1) * NB, vnext, 0);
-              TMEM_LD16(tbase_addr + (bh + 1) * NB + 16, vnext, 16);
-            } else {
+            if (bp + 1 == kTile / (2 * NB)) {
               tc_fence_before();
               __syncwarp();
               if (lane == 0) mbar_arrive(acce0 + 8 * a);
             }
             if constexpr (kMask) {
-              const int tbase = t0 + bh * NB;
+              const int tbase = t0 + bp * 2 * NB;
 #pragma unroll
-              for (int j = 0; j < NB; ++j) v[j] = (tbase + j > limit1) ? -INFINITY : v[j];
+              for (int j = 0; j < 2 * NB; ++j) vp[j] = (tbase + j > limit1) ? -INFINITY : vp[j];
             }
-            // online softmax normaliser: batch max (3-input FMNMX), branch-free rescale
-            float mx = max3f(v[0], v[1], v[2]);
-#pragma unroll
-            for (int j = 3; j < NB - 1; j += 2) mx = max3f(mx, v[j], v[j + 1]);
-            mx = fmaxf(mx, v[NB - 1]);
-            const float mn = fmaxf(m, mx * scale);              // -inf only if nothing valid yet
-            const float mref = mn > -INFINITY ? mn : 0.f;
-            const float rescale = ex2f(m - mref);               // m = -inf -> 0 (ssum is 0 anyway)
-            const float bsum = sum_exp_n<NB>(v, scale, mref);
-            ssum = ssum * rescale + bsum;
-            m = mn;
+            online(vp, m, ssum);
+            online(vp + NB, m1, s1);
           };
+          // warp-uniform: G*w = 32*G, so a warp's 32 columns are all valid or all padding
           if (!warp_cols) {
             // padding warp (columns >= G*w): only the accumulator release
             tc_fence_before();
@@ -810,16 +832,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
             if (lane == 0) mbar_arrive(acce0 + 8 * a);
           } else if (!need_mask) {
 #pragma unroll 1
-            for (int bh = 0; bh < kTile / NB; bh += 2) {
-              batch(va, vb2, bh, std::false_type{});
-              batch(vb2, va, bh + 1, std::false_type{});
-            }
+            for (int bp = 0; bp < kTile / (2 * NB); ++bp) pair(bp, std::false_type{});
           } else {
 #pragma unroll 1
-            for (int bh = 0; bh < kTile / NB; bh += 2) {
-              batch(va, vb2, bh, std::true_type{});
-              batch(vb2, va, bh + 1, std::true_type{});
-            }
+            for (int bp = 0; bp < kTile / (2 * NB); ++bp) pair(bp, std::true_type{});
           }
         } else {
           // ---- pass 2: this thread owns token t and the W/2 window rows of its half. The MMA
@@ -831,7 +847,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
 #pragma unroll
           for (int k = 0; k < K::HC / 16; ++k) TMEM_LD16(lane_base + a * 256 + half * K::HC + k * 16, v, k * 16);
           tmem_wait_ld();
-          const unsigned long long ts1 = (c.debug & 1u) ? gtimer() : 0ull;
+          const uint32_t ts1 = (c.debug & 1u) ? (uint32_t)gtimer() : 0u;
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(acce0 + 8 * a);       // accumulator free for MMA(astep + 2)
@@ -855,14 +871,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
           const float accs = (acc[0] + acc[1]) + (acc[2] + acc[3]);
           float* cb = comb + (astep & 1) * kTile;
           if (half == 1) cb[q * 32 + lane] = accs;
-          if (c.debug & 1u) { const unsigned long long ts2 = gtimer(); tacc[3] += ts1 - ts0; tacc[4] += ts2 - ts1; }
+          if (c.debug & 1u) { const uint32_t ts2 = (uint32_t)gtimer(); tacc[3] += ts1 - ts0; tacc[4] += ts2 - ts1; }
           named_bar(1, kEpiWarps * 32);
           if (half == 0 && t < u.T && !(c.debug & 16384u))
             c.ws.scores[(size_t)unit * c.max_seq_len + t] = (accs + cb[q * 32 + lane]) * (1.0f / W);
         }
         if (rec) dbg[8192 + astep * 4 + 2] = gtimer();
         if (c.debug & 1u) {
-          const unsigned long long te = gtimer();
+          const uint32_t te = (uint32_t)gtimer();
           if (i < u.nt) { tacc[0] += te - ts0; tacc[1] += 1; } else { tacc[6] += te - ts0; tacc[7] += 1; }
           tlast = te;
         }

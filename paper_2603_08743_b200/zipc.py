@@ -10,7 +10,8 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libzipc.so")
+# ZPC_LIB: an alternative build of the same library (A/B timing of two builds on one GPU box)
+LIB_PATH = os.environ.get("ZPC_LIB") or os.path.join(HERE, "lib", "libzipc.so")
 
 ZPC_OK = 0
 ZPC_ERR_INVALID_ARG = -1

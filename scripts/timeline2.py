@@ -65,3 +65,7 @@ print("loader warps: start (after stage free) .. end (copies issued) per warp [k
 for g in list(range(180, 192)):
     st = LW[g, 0:4] - t0; en = LW[g, 8:12] - t0
     print(f"{g:4d} P{1 + ((g % (2*npass)) >= npass)} start " + " ".join(f"{x:8.2f}" for x in st) + " | issue dur " + " ".join(f"{x:5.2f}" for x in (en - st)) + f" | full {M[g,2]-t0:8.2f}")
+RL = raw[40960:40960 + 2048].reshape(1024, 2) / 1e3
+print("relay: step | relay start wait  | accf seen | MMA issued(M3) | epi barrier exit (E1) | epi prev done (E2[g-1])")
+for g in list(range(150, 160)) + list(range(176, 184)):
+    print(f"{g:4d} P{1 + ((g % (2*npass)) >= npass)} {RL[g,0]-t0:9.2f} {RL[g,1]-t0:9.2f} {M[g,3]-t0:9.2f} {E[g,1]-t0:9.2f} {E[g-1,2]-t0:9.2f}")
