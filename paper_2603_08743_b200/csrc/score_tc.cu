@@ -575,18 +575,49 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
       mbar_wait_backoff(idf0 + 8 * slot, (ld_step / kIdSlots) & 1, 100);
       // all block ids first (explicit ld.shared: a generic load would queue behind the copies)
       const uint32_t sid = ids_base + (uint32_t)slot * kMaxIds * 4;
-      uint32_t off[kTile / RPP];
+      if (c.b == 16 && !(c.debug & 256u)) {
+        // block-major fast path (b = 16): one id per block, this thread's 16/RPP rows of the block
+        // at a constant stride -- few instructions per cp.async (the gather shares its SMSPs with
+        // the MUFU-bound epilogue, so its instruction count is its throughput; measured)
+        constexpr int RB = 16 / RPP;                         // rows of a block per thread
+        constexpr int NBLK = kTile / 16;
+        const uint32_t qstride = (uint32_t)RPP * hD;
+        const uint32_t rbase = (uint32_t)rsub * hD;
+        int blk[NBLK];
 #pragma unroll
-      for (int k = 0; k < kTile / RPP; ++k) {
-        const int t = t0 + RPP * k + rsub;
-        const int jr = b_pow2 ? (t >> b_log2) : t / c.b;
-        const int blk = lds_s32(sid + 4u * (uint32_t)min(max(jr - j0, 0), kMaxIds - 1));
-        off[k] = ((uint32_t)blk * (uint32_t)c.b + (uint32_t)(t - jr * c.b)) * hD;
-      }
-      if (!(c.debug & 256u)) {
+        for (int jb = 0; jb < NBLK; ++jb) blk[jb] = lds_s32(sid + 4u * (uint32_t)jb);
+        if (t0 + kTile <= T) {                               // full tile: no predicates
 #pragma unroll
-        for (int k = 0; k < kTile / RPP; ++k)
-          if (t0 + RPP * k + rsub < T) cp_async16(dst0 + (uint32_t)(RPP * k * 128), lbase + off[k]);
+          for (int jb = 0; jb < NBLK; ++jb) {
+            uint32_t off = (uint32_t)blk[jb] * 16u * hD + rbase;
+#pragma unroll
+            for (int q = 0; q < RB; ++q, off += qstride)
+              cp_async16(dst0 + (uint32_t)((jb * 16 + q * RPP) * 128), lbase + off);
+          }
+        } else {
+#pragma unroll
+          for (int jb = 0; jb < NBLK; ++jb) {
+            uint32_t off = (uint32_t)blk[jb] * 16u * hD + rbase;
+#pragma unroll
+            for (int q = 0; q < RB; ++q, off += qstride)
+              if (t0 + jb * 16 + q * RPP + rsub < T)
+                cp_async16(dst0 + (uint32_t)((jb * 16 + q * RPP) * 128), lbase + off);
+          }
+        }
+      } else {
+        uint32_t off[kTile / RPP];
+#pragma unroll
+        for (int k = 0; k < kTile / RPP; ++k) {
+          const int t = t0 + RPP * k + rsub;
+          const int jr = b_pow2 ? (t >> b_log2) : t / c.b;
+          const int blk = lds_s32(sid + 4u * (uint32_t)min(max(jr - j0, 0), kMaxIds - 1));
+          off[k] = ((uint32_t)blk * (uint32_t)c.b + (uint32_t)(t - jr * c.b)) * hD;
+        }
+        if (!(c.debug & 256u)) {
+#pragma unroll
+          for (int k = 0; k < kTile / RPP; ++k)
+            if (t0 + RPP * k + rsub < T) cp_async16(dst0 + (uint32_t)(RPP * k * 128), lbase + off[k]);
+        }
       }
       cp_async_arrive_noinc(full0 + 8 * st);
       __syncwarp();
