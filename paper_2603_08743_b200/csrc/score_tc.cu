@@ -33,12 +33,11 @@ namespace zpc {
 namespace {
 
 constexpr int kTile = 128;       // tokens per tile (UMMA M in pass 2, N in pass 1)
-constexpr int kThreads = 512;    // 16 warps: Q-TMA, MMA, table walker, spare, 4 K loaders, 8 epilogue
+constexpr int kThreads = 512;    // 16 warps: Q-TMA, MMA, (idle), feeder, 4 K loaders, 8 epilogue
 constexpr int kLoadWarps = 4;
 constexpr int kEpiWarp0 = 8;     // first epilogue warp (warps 8..15: lane quarter = warp % 4)
 constexpr bool kPolyOffload = false;   // 25% of pass-1 exp2 on the FMA pipe (pays off only when MUFU-bound)
-constexpr int kIdSlots = 8;      // block-id ring (steps) filled by the walker, 4 steps per group
-constexpr int kIdGroup = 4;
+constexpr int kIdSlots = 2;      // block ids of the tile being gathered (double-buffered, feeder warp)
 constexpr int kMaxIds = 32;      // block ids per 128-token tile (b >= 5)
 constexpr int kEpiWarps = 8;
 // setmaxnreg budget: 8 producer warps x kProdRegs + 8 epilogue warps x kEpiRegs <= 64K registers
@@ -393,7 +392,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + K::OFF_BAR);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 54);
   int* ids = reinterpret_cast<int*>(smem + K::OFF_IDS);                  // [kIdSlots][kMaxIds]
-  const uint32_t idf0 = smem_u32(bars + 24), ide0 = smem_u32(bars + 32);  // ids full / empty
   const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + 40);
   const uint32_t accf0 = smem_u32(bars + 8), acce0 = smem_u32(bars + 10);
   const uint32_t qfull0 = smem_u32(bars + 12), qempty0 = smem_u32(bars + 14);
@@ -415,7 +413,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
       mbar_init(qempty0 + 8 * a, 1);
       mbar_init(xchg0 + 8 * a, C);
     }
-    for (int k = 0; k < kIdSlots; ++k) { mbar_init(idf0 + 8 * k, 1); mbar_init(ide0 + 8 * k, kLoadWarps); }
     mbar_init(augf, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -485,52 +482,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
       }
     }
     __syncwarp();
-  } else if (warp == 2 && (c.debug & 2048u)) {
-    // bisection: no walker
   } else if (warp >= 4 && warp < 4 + kLoadWarps && (c.debug & 2048u)) {
-    // bisection: no loaders
-  } else if (warp == 2) {
-    // ================= table walker: block ids of every K tile, kIdGroup steps at a time, into a
-    // shared ring, so the gathering threads never wait on a table load (DESIGN.md §Score kernel)
-    int w_unit = cluster_id, w_i = 0, g = 0;
-    UnitInfo w_u = w_unit < units ? unit_info(w_unit) : UnitInfo{};
-    while (true) {
-      int gs = 0;
-      int t0s[kIdGroup], js[kIdGroup], nbs[kIdGroup];
-      const int* tbl[kIdGroup];
-#pragma unroll
-      for (int k = 0; k < kIdGroup; ++k) {
-        while (w_unit < units && w_i >= 2 * w_u.nt) {
-          w_unit += nclusters;
-          w_i = 0;
-          if (w_unit < units) w_u = unit_info(w_unit);
-        }
-        nbs[k] = 0;
-        if (w_unit < units) {
-          t0s[k] = tile_of(w_u, w_i) * kTile;
-          js[k] = t0s[k] / c.b;
-          nbs[k] = (min(t0s[k] + kTile, w_u.T) - 1) / c.b - js[k] + 1;
-          tbl[k] = c.tables + (size_t)w_u.r * c.table_stride;
-          ++w_i;
-          ++gs;
-        }
-      }
-      if (gs == 0) break;
-      int v[kIdGroup];
-#pragma unroll
-      for (int k = 0; k < kIdGroup; ++k) v[k] = (k < gs && lane < nbs[k]) ? __ldg(tbl[k] + js[k] + lane) : 0;
-#pragma unroll
-      for (int k = 0; k < kIdGroup; ++k) {
-        if (k < gs) {
-          const int slot = (g + k) % kIdSlots;
-          mbar_wait_backoff(ide0 + 8 * slot, (((g + k) / kIdSlots) & 1) ^ 1, 200);
-          ids[slot * kMaxIds + lane] = v[k];
-          __syncwarp();
-          if (lane == 0) mbar_arrive(idf0 + 8 * slot);
-        }
-      }
-      g += gs;
-    }
+    // bisection: no loaders (the feeder is off too)
   } else if (warp >= 4 && warp < 4 + kLoadWarps) {
     // ---- K gather by the loader warps: rows through the block table (ids from the walker), 16-B
     // cp.async each (D/8 threads per 2*D-byte row, coalesced), written straight into the SW128
@@ -561,7 +514,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
       }
       if (ld_unit >= units) return;
       const int st = ld_step % K::ST;
-      const int slot = ld_step % kIdSlots;
       const int t0 = tile_of(ld_u, ld_i) * kTile;
       const int j0 = b_pow2 ? (t0 >> b_log2) : t0 / c.b;
       const int T = ld_u.T;
@@ -572,9 +524,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
         reinterpret_cast<unsigned long long*>(c.ws.kept)[4096 + ld_step * 16 + (warp - 4)] = gtimer();
       if ((c.debug & 1u) && blockIdx.x == 0 && et == 0 && ld_step < 512)
         reinterpret_cast<unsigned long long*>(c.ws.kept)[ld_step * 4 + 0] = gtimer();
-      mbar_wait_backoff(idf0 + 8 * slot, (ld_step / kIdSlots) & 1, 100);
+      named_bar(4, kLoadWarps * 32 + 32);                     // feeder: ids of this tile, stage free
       // all block ids first (explicit ld.shared: a generic load would queue behind the copies)
-      const uint32_t sid = ids_base + (uint32_t)slot * kMaxIds * 4;
+      const uint32_t sid = ids_base + (uint32_t)(ld_step & 1) * kMaxIds * 4;
       if (c.b == 16 && !(c.debug & 256u)) {
         // block-major fast path (b = 16): one id per block, this thread's 16/RPP rows of the block
         // at a constant stride -- few instructions per cp.async (the gather shares its SMSPs with
@@ -620,47 +572,48 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
         }
       }
       cp_async_arrive_noinc(full0 + 8 * st);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(ide0 + 8 * slot);
       if ((c.debug & 1u) && blockIdx.x == 0 && lane == 0 && ld_step < 256)
         reinterpret_cast<unsigned long long*>(c.ws.kept)[4096 + ld_step * 16 + 8 + (warp - 4)] = gtimer();
       ++ld_i;
       ++ld_step;
     };
-    for (int g = 0; ; ++g) {
-      if (ld_unit >= units) break;
-      if (g >= K::ST) {   // stage reuse: wait for the MMAs that read it
-        const int st = g % K::ST;
-        mbar_wait_backoff(empty0 + 8 * st, ((g / K::ST) & 1) ^ 1, 100);
-      }
-      issue_next_load();
-    }
+    while (ld_unit < units) issue_next_load();
 
-  } else if (warp == 3) {
-    // ================= relay: each step's MMA completion (commit mbarrier) is passed to the
-    // epilogue through a hardware named barrier (bar.arrive), so the 256 epilogue threads block in
-    // bar.sync instead of polling; kept off the MMA warp so MMA(k) issues without waiting for
-    // MMA(k-1) to finish (back-to-back on the tensor pipe; measured: pass 2 was MMA-serialised).
-    // Barrier reuse is safe: MMA(k+2) needs acc_empty(k), i.e. every epilogue warp past barrier k.
-    int astep = 0;
-    for (int unit = cluster_id; unit < units; unit += nclusters) {
-      const UnitInfo u = unit_info(unit);
-      for (int i = 0; i < 2 * u.nt; ++i, ++astep) {
-        const bool rrec = (c.debug & 1u) && blockIdx.x == 0 && lane == 0 && astep < 1024;
-        unsigned long long* rdbg = reinterpret_cast<unsigned long long*>(c.ws.kept) + 40960;
-        if (rrec) rdbg[astep * 2 + 0] = gtimer();
-        if (lane == 0) mbar_wait(accf0 + 8 * (astep & 1), (astep >> 1) & 1);
-        __syncwarp();
-        if (rrec) rdbg[astep * 2 + 1] = gtimer();
-        if (c.debug & 8u) named_bar_arrive(2 + (astep & 1), (kEpiWarps + 1) * 32);
+  } else if (warp == 3 && !(c.debug & 2048u)) {
+    // ================= feeder: for every K tile, in the loaders' order, the block ids (one table
+    // load per lane, issued before the wait so its latency overlaps it) and the stage's release by
+    // the MMA (the empty mbarrier, polled here only); then one named barrier with the 128
+    // gathering threads publishes both. The loaders block in bar.sync instead of polling (their
+    // polls cost issue slots on SMSPs the MUFU-bound epilogue shares; measured). bar.sync on both
+    // sides keeps the feeder from running ahead; ids are double-buffered (slot g & 1 is rewritten
+    // only after every loader has passed barrier g + 1, i.e. finished reading tile g's ids).
+    int f_unit = cluster_id, f_i = 0;
+    UnitInfo f_u = f_unit < units ? unit_info(f_unit) : UnitInfo{};
+    for (int g = 0;; ++g) {
+      while (f_unit < units && f_i >= 2 * f_u.nt) {
+        f_unit += nclusters;
+        f_i = 0;
+        if (f_unit < units) f_u = unit_info(f_unit);
       }
+      if (f_unit >= units) break;
+      const int t0 = tile_of(f_u, f_i) * kTile;
+      const int j0 = t0 / c.b;
+      const int nb = (min(t0 + kTile, f_u.T) - 1) / c.b - j0 + 1;
+      const int v = lane < nb ? __ldg(c.tables + (size_t)f_u.r * c.table_stride + j0 + lane) : 0;
+      if (g >= K::ST) {   // stage reuse: the MMAs that read it are complete
+        if (lane == 0) mbar_wait(empty0 + 8 * (g % K::ST), ((g / K::ST) & 1) ^ 1);
+        __syncwarp();
+      }
+      ids[(g & 1) * kMaxIds + lane] = v;
+      named_bar(4, kLoadWarps * 32 + 32);
+      ++f_i;
     }
   } else if (warp == 1) {
     // ================= MMA issuer: the whole warp runs converged (descriptors are warp-uniform,
     // so ptxas keeps them in uniform registers) and one elected lane issues each tcgen05.mma /
     // commit; a lane-0-only region made ptxas wrap every MMA in an ELECT/R2UR/BRA.U.ANY loop
     // (~100 cycles per issue, measured: the 9-MMA pass-2 step could not keep the tensor pipe fed).
-    // Completion is relayed to the epilogue by warp 3.
+    // Each epilogue warp waits the commit mbarrier of its step itself.
     int kstep = 0, astep = 0;
     const uint64_t aug_a = none_desc(smem_u32(smem + K::OFF_AUG_A), 128, 256);
     const uint64_t aug_b = none_desc(smem_u32(smem + K::OFF_AUG_B), 128, 256);
@@ -792,8 +745,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
         // MMA(astep) complete: each warp waits the commit mbarrier itself (try_wait parks the warp;
         // no cross-warp barrier, so warps are not held to the slowest one every step). No phase
         // aliasing: MMA(astep + 2) needs every epilogue warp's acc_empty arrival for astep.
-        if (c.debug & 8u) named_bar(2 + a, (kEpiWarps + 1) * 32);   // bisection: relay-warp barrier
-        else mbar_wait(accf0 + 8 * a, (astep >> 1) & 1);
+        mbar_wait(accf0 + 8 * a, (astep >> 1) & 1);
         if (rec) dbg[8192 + astep * 4 + 1] = gtimer();
         const uint32_t ts0 = (c.debug & 1u) ? (uint32_t)gtimer() : 0u;   // per-warp register timing (mod 2^32)
         if (c.debug & 1u) { tacc[(i < u.nt ? 0 : 3) + 2] += ts0 - tlast; }
