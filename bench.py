@@ -172,6 +172,29 @@ def max_over_ranks(value, dist=None, device=None):
     return float(t.item())
 
 
+# ---------------------------------------------------------------- measured DRAM traffic
+TRAFFIC_FILE = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_traffic.json")
+
+
+def measured_traffic(cfg, per_gpu):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu --set full capture
+    of this exact workload (profiles/r01_traffic.json: the full qwen7b batch, 64 requests), else {}."""
+    if cfg.name != "qwen7b" or per_gpu != 64 or not os.path.exists(TRAFFIC_FILE):
+        return {}
+    try:
+        kern = json.load(open(TRAFFIC_FILE))["kernels"]
+    except (OSError, ValueError, KeyError):
+        return {}
+    out = {}
+    for name, rec in kern.items():
+        tot = rec["dram_bytes_read"] + rec["dram_bytes_write"]
+        if f"k_score_tc<{cfg.h_q // cfg.h_kv}, {cfg.w}, {cfg.d}," in name:
+            out["score"] = tot
+        elif "k_compact" in name:
+            out["compact"] = tot
+    return out
+
+
 # ---------------------------------------------------------------- GPU arm
 def algorithmic_bytes(cfg, seq_lens, budgets, moves):
     """SURVEY §8(d) per-unit algorithmic bytes summed over the batch."""
@@ -321,8 +344,10 @@ def main():
     score_ms = stage_ms[1] / args.steps
     compact_ms = stage_ms[3] / args.steps
     step_bytes = ab["score"] + ab["select"] + ab["compact"]
+    traffic = measured_traffic(cfg, per_gpu)
     roofline = {"kernel": "score (a1+a2)", "bound": "hbm", "achieved": ab["score"] / (score_ms / 1e3) / 1e9,
-                "peak": peaks["hbm"], "unit": "GB/s", "peak_src": peaks["src"], "traffic": None,
+                "peak": peaks["hbm"], "unit": "GB/s", "peak_src": peaks["src"],
+                "traffic": traffic.get("score"), "traffic_unit": "bytes/launch (dram read+write, ncu --set full)",
                 "algorithmic_bytes_per_launch": ab["score"]}
     roofline["frac"] = roofline["achieved"] / roofline["peak"]
     tensor_tf = ab["flops_score"] * 2 / (score_ms / 1e3) / 1e12   # two passes of 2*G*w*d per token
@@ -331,7 +356,8 @@ def main():
         "score_tensor_tflops_two_pass": tensor_tf,
         "compact_roofline": {"achieved": ab["compact"] / (compact_ms / 1e3) / 1e9 if compact_ms else None,
                              "peak": peaks["hbm"], "unit": "GB/s", "moved_rows": moves,
-                             "frac": (ab["compact"] / (compact_ms / 1e3) / 1e9) / peaks["hbm"] if compact_ms else None},
+                             "frac": (ab["compact"] / (compact_ms / 1e3) / 1e9) / peaks["hbm"] if compact_ms else None,
+                             "traffic": traffic.get("compact"), "algorithmic_bytes_per_launch": ab["compact"]},
         "step_hbm_frac": step_bytes / (ms_per_step / 1e3) / 1e9 / peaks["hbm"],
         "kv_tokens_per_s": T_sum * world / (ms_per_step / 1e3),
         "wall_s_incl_restores": wall,
