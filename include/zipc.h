@@ -44,13 +44,15 @@
 extern "C" {
 #endif
 
-#define ZPC_ABI_VERSION 1
+#define ZPC_ABI_VERSION 2
 
 /* ---- return / status codes ---- */
 #define ZPC_OK                  0
 #define ZPC_ERR_INVALID_ARG    -1   /* bad descriptor/params: even pool_kernel, w<1, n_max<2,
                                        unsupported head_dim/dtype, h_q not a multiple of h_kv,
-                                       G*w > 256, max_seq_len above the select limit, NULL pointer */
+                                       G*w > 256, max_seq_len above the select limit, NULL pointer,
+                                       ZPC_F_REDUNDANCY with lambda < 0, tau <= 0, p outside [0,1],
+                                       a non-finite value or block_size > 32 */
 #define ZPC_ERR_WORKSPACE      -2   /* workspace_bytes < zpc_workspace_bytes(...) */
 #define ZPC_ERR_CUDA           -3   /* a launch failed (cudaGetLastError) */
 #define ZPC_ERR_NOT_TRIGGERED -10   /* device: N = ceil(T/b) < N_max */
@@ -76,6 +78,10 @@ extern "C" {
 #define ZPC_F_VALIDATE    2u  /* also reject duplicate block ids inside a table */
 #define ZPC_F_COUNT_MOVES 4u  /* count moved rows into the workspace counter (bytes accounting) */
 #define ZPC_F_SCORE_CUDACORE 8u /* force the CUDA-core scoring kernel even for bf16 (testing) */
+#define ZPC_F_REDUNDANCY 16u  /* NEXT-1: lightning redundancy score (§C.7) with the
+                                 temperature softmax (§C.8) folded into the selection
+                                 score after pooling: S = MaxPool(S) - lambda * softmax(r / tau)
+                                 (PAPER.md:506). Uses params.redundancy_*; adds a workspace region. */
 
 /* Pool geometry: K, V [L][N_total][b][h_kv][d], Q [L][M][w][h_q][d].
  * Q row u of slot j holds the query of position T-w+u of the request bound to slot j (R3). */
@@ -96,6 +102,15 @@ typedef struct {
   int32_t pool_kernel;   /* 1 = no pooling; odd >= 3 = MaxPool1D width, stride 1, same length (R6) */
   int32_t max_seq_len;   /* host bound on seq_lens: sizes the workspace and grids (<= ZPC_MAX_SEQ_LEN) */
   uint32_t flags;        /* ZPC_F_* */
+  /* ZPC_F_REDUNDANCY only (ignored otherwise; all finite):
+   *   redundancy_lambda  lambda >= 0, weight of R in S - lambda*R (PAPER.md:506; 0.2 recommended, :718)
+   *   redundancy_tau     tau > 0, temperature of the softmax over the sequence (0.4)
+   *   redundancy_p       p in [0, 1], similarity threshold: per column of a block's cosine matrix
+   *                      the last (newest-row) entry strictly above p is zeroed (
+   *                      the paper gives no value) */
+  float redundancy_lambda;
+  float redundancy_tau;
+  float redundancy_p;
 } zpc_params;
 
 #define ZPC_MAX_SEQ_LEN 49152   /* select keeps a unit's scores in shared memory */
@@ -149,6 +164,8 @@ typedef struct {
   size_t n_prefix;   /* int32 [R] */
   size_t lse;        /* fp32 [R][L][h_kv][G*w]: log2-domain log-sum-exp per window row/head */
   size_t moves;      /* unsigned long long [1]: rows moved (ZPC_F_COUNT_MOVES) */
+  size_t redundancy; /* fp32 [R][L][h_kv][max_seq_len]: lightning row sums r[t] / T before the
+                        softmax (ZPC_F_REDUNDANCY; a zero-size region otherwise) */
   size_t internal;   /* library-private scratch */
   int32_t kept_stride;   /* (N_max-1)*b */
 } zpc_workspace_layout;
@@ -164,10 +181,16 @@ int zpc_compress(const zpc_cache_desc* desc, const zpc_params* params, const zpc
 /* Stage entry points (same conventions; each consumes the previous stage's workspace output).
  * zpc_plan writes *status, targets/reserved/n_prefix and the internal scan; it mutates nothing
  * outside the workspace and *status. zpc_score writes S and LSE. zpc_select writes kept and
- * new_lens. zpc_compact moves K/V rows. zpc_finalize rewrites tables, ref counts, freed list,
+ * new_lens (with ZPC_F_REDUNDANCY it reads the `redundancy` region written by zpc_redundancy).
+ * zpc_compact moves K/V rows. zpc_finalize rewrites tables, ref counts, freed list,
  * free stack and top, new_num_blocks. */
 int zpc_plan(const zpc_cache_desc* desc, const zpc_params* params, const zpc_batch* batch, void* stream);
 int zpc_score(const zpc_cache_desc* desc, const zpc_params* params, const zpc_batch* batch, void* stream);
+/* NEXT-1 stage (ZPC_F_REDUNDANCY): per unit and block of b tokens, the b x b cosine similarity of
+ * the block's keys (diagonal zeroed, per column the last entry > p zeroed), row sums / T into the
+ * workspace `redundancy` region; slots >= T take no part, a zero-norm key has cosine 0. A no-op
+ * (returns ZPC_OK) when the flag is clear. zpc_select then folds lambda * softmax(r / tau) in. */
+int zpc_redundancy(const zpc_cache_desc* desc, const zpc_params* params, const zpc_batch* batch, void* stream);
 int zpc_select(const zpc_cache_desc* desc, const zpc_params* params, const zpc_batch* batch, void* stream);
 int zpc_compact(const zpc_cache_desc* desc, const zpc_params* params, const zpc_batch* batch, void* stream);
 int zpc_finalize(const zpc_cache_desc* desc, const zpc_params* params, const zpc_batch* batch, void* stream);

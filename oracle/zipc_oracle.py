@@ -35,6 +35,7 @@ ERR_CAPACITY = -16
 
 F_PREFIX = 1
 F_VALIDATE = 2
+F_REDUNDANCY = 16   # NEXT-1: lightning redundancy + temperature softmax + S - lambda*R
 
 
 @dataclass
@@ -61,6 +62,9 @@ class Params:
     pool_kernel: int = 1
     max_seq_len: int = 1 << 30
     flags: int = 0
+    lam: float = 0.2      # lambda, PAPER.md:718 (§C.8 recommended)
+    tau: float = 0.4      # tau
+    sim_p: float = 0.8    # similarity threshold p: no value in the paper (R19)
 
 
 # --------------------------------------------------------------------------
@@ -284,6 +288,75 @@ def pin_window(s: np.ndarray, T: int, w: int) -> np.ndarray:
 
 
 # --------------------------------------------------------------------------
+# NEXT-1: lightning redundancy, temperature softmax, S - lambda*R
+#   PAPER.md:498-507 (§C.5, redundancy score + Eq. S = S - lambda R), :616-620 (§C.7 lightning
+#   redundancy: similarity only between keys of the same block), :677 (§C.8 temperature tau)
+# Readings: R19 p is a parameter (no value in the paper); R20 "normalized by the
+# sequence length" divides by T and slots >= T take no part; R21 "exceeding" is strictly greater,
+# the diagonal is zeroed first, "last" is the largest row index (newest token); R22 combine after
+# pooling, before the pin, tau only in the redundancy softmax; R23 a zero-norm key has cosine 0.
+# --------------------------------------------------------------------------
+def cosine_matrix(keys: np.ndarray) -> np.ndarray:
+    """Cosine similarity of every pair of key rows (fp64), zero-norm rows -> 0 (R23)."""
+    n = np.sqrt((keys * keys).sum(axis=1))
+    safe = np.where(n > 0, n, 1.0)
+    C = (keys @ keys.T) / safe[:, None] / safe[None, :]
+    C[n == 0, :] = 0.0
+    C[:, n == 0] = 0.0
+    return C
+
+
+def redundancy_raw_masked(keys: np.ndarray, mask: np.ndarray, p: float) -> np.ndarray:
+    """The redundancy computation of PAPER.md:502 on the similarity entries allowed by `mask`
+    ([T, T] bool): diagonal zeroed, per column the LAST (largest row index) entry > p zeroed,
+    row sums, divided by the sequence length T. mask = all-True is the paper's original (naive)
+    score; the block-diagonal mask is the lightning score."""
+    T = keys.shape[0]
+    C = np.where(mask, cosine_matrix(keys), 0.0)
+    np.fill_diagonal(C, 0.0)
+    for j in range(T):
+        above = np.nonzero(C[:, j] > p)[0]
+        if len(above):
+            C[above[-1], j] = 0.0
+    return C.sum(axis=1) / T
+
+
+def lightning_redundancy_raw(keys: np.ndarray, b: int, p: float) -> np.ndarray:
+    """Lightning redundancy, written per block of b tokens (the last block may
+    be partial: only the T valid tokens take part, R20)."""
+    T = keys.shape[0]
+    r = np.zeros(T)
+    for j0 in range(0, T, b):
+        blk = keys[j0:min(T, j0 + b)]
+        C = cosine_matrix(blk)
+        np.fill_diagonal(C, 0.0)
+        for j in range(C.shape[1]):
+            above = np.nonzero(C[:, j] > p)[0]
+            if len(above):
+                C[above[-1], j] = 0.0
+        r[j0:j0 + len(blk)] = C.sum(axis=1)
+    return r / T
+
+
+def softmax_temperature(x: np.ndarray, tau: float) -> np.ndarray:
+    """softmax(x / tau) over the sequence, max-subtracted."""
+    z = x / tau
+    e = np.exp(z - z.max())
+    return e / e.sum()
+
+
+def combine_redundancy(s_pooled: np.ndarray, r_raw: np.ndarray, lam: float, tau: float) -> np.ndarray:
+    """S = S - lambda * R with R = softmax(r_raw / tau) (PAPER.md:506, :677)."""
+    return s_pooled - lam * softmax_temperature(r_raw, tau)
+
+
+def unit_keys(geo: Geometry, k_pool_f64, table, T: int, l: int, h: int) -> np.ndarray:
+    """The unit's T key rows in logical order (gathered through the block table)."""
+    t = np.arange(T)
+    return k_pool_f64[l, np.asarray(table)[t // geo.b], t % geo.b, h]
+
+
+# --------------------------------------------------------------------------
 # a4: per-head top-l with the index tie rule — PAPER.md:85, :591 (§C.6)
 # --------------------------------------------------------------------------
 def select(s_final: np.ndarray, ell: int) -> np.ndarray:
@@ -409,6 +482,7 @@ class CompressOut:
     kept: dict = None                # (r, l, h) -> ascending kept positions
     scores: dict = None              # (r, l, h) -> raw s (pre-pool) fp64
     fin: FinalizeOut = None
+    redundancy: dict = None          # (r, l, h) -> lightning r_raw (pre-softmax) fp64 (F_REDUNDANCY)
     plan: Plan = None
 
 
@@ -431,7 +505,7 @@ def compress(geo: Geometry, prm: Params, k_cache, v_cache, q_cache, q_slots, seq
     qf = widen(q_cache, geo.dtype)
     kf = widen(k_cache, geo.dtype)
     new_lens = np.zeros((R, geo.L, geo.h_kv), np.int32)
-    kept_all, scores = {}, {}
+    kept_all, scores, redund = {}, {}, {}
     for r in range(R):
         T = int(seq_lens[r])
         for l in range(geo.L):
@@ -446,7 +520,12 @@ def compress(geo: Geometry, prm: Params, k_cache, v_cache, q_cache, q_slots, seq
                         continue
                     s = unit_scores(geo, qf, kf, tables[r], T, int(q_slots[r]), l, h, blockwise)
                     scores[key] = s
-                    kept = select(pin_window(max_pool(s, prm.pool_kernel), T, geo.w), ell)
+                    sp = max_pool(s, prm.pool_kernel)
+                    if prm.flags & F_REDUNDANCY:
+                        rr = lightning_redundancy_raw(unit_keys(geo, kf, tables[r], T, l, h), geo.b, prm.sim_p)
+                        redund[key] = rr
+                        sp = combine_redundancy(sp, rr, prm.lam, prm.tau)
+                    kept = select(pin_window(sp, T, geo.w), ell)
                 kept_all[key] = kept
     for r in range(R):
         N = int(pl.n_blocks[r])
@@ -458,4 +537,4 @@ def compress(geo: Geometry, prm: Params, k_cache, v_cache, q_cache, q_slots, seq
                 compact_gather(k_out[l], v_out[l], tables[r], pl.targets[r], kept_all[key], h, geo.b)
     fin = finalize(geo, prm, pl, tables, ref_counts, free_stack, free_top)
     return CompressOut(status=OK, k_cache=k_out, v_cache=v_out, new_lens=new_lens, kept=kept_all,
-                       scores=scores, fin=fin, plan=pl)
+                       scores=scores, fin=fin, plan=pl, redundancy=redund)

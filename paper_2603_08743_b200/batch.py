@@ -11,13 +11,18 @@ import torch
 from . import zipc
 
 
-def desc_params(w, flags=0, pool_kernel=None, max_seq_len=None):
+def desc_params(w, flags=0, pool_kernel=None, max_seq_len=None, redundancy=None):
+    """redundancy: None, or (lambda, tau, p) -> sets ZPC_F_REDUNDANCY with those parameters."""
     cfg, lay = w.cfg, w.layout
     desc = zipc.make_desc(cfg.L, cfg.h_kv, cfg.h_q, cfg.d, cfg.b, lay.N_total, lay.M, cfg.w, cfg.dtype)
     if w.ref_counts is not None:
         flags |= zipc.ZPC_F_PREFIX
+    extra = {}
+    if redundancy is not None:
+        flags |= zipc.ZPC_F_REDUNDANCY
+        extra = dict(redundancy_lambda=redundancy[0], redundancy_tau=redundancy[1], redundancy_p=redundancy[2])
     params = zipc.make_params(cfg.n_max, cfg.pool_kernel if pool_kernel is None else pool_kernel,
-                              int(max_seq_len or w.max_seq_len), flags)
+                              int(max_seq_len or w.max_seq_len), flags, **extra)
     return desc, params
 
 

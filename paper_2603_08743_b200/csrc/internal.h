@@ -15,6 +15,7 @@ struct Ws {
   int32_t* n_prefix;       // [R]
   float* lse;              // [R][L][h_kv][G*w]
   unsigned long long* moves;
+  float* redund;           // [R][L][h_kv][max_seq_len] lightning r[t] / T (ZPC_F_REDUNDANCY)
   // internal
   int32_t* req_err;        // [R]
   int32_t* n_blocks;       // [R]
@@ -31,6 +32,7 @@ struct Call {
   int32_t n_max, pool_kernel, max_seq_len;
   uint32_t flags;
   uint32_t debug;      // tuning/bisection switches (ZPC_SCORE_DEBUG), 0 in production
+  float red_lambda, red_tau, red_p;   // ZPC_F_REDUNDANCY parameters
   int32_t R, table_stride, free_capacity, freed_capacity;
   void* k_cache;
   void* v_cache;
@@ -66,6 +68,7 @@ cudaError_t launch_score_cudacore(const Call& c, cudaStream_t s);
 cudaError_t launch_score_tc(const Call& c, cudaStream_t s, bool* used);
 cudaError_t launch_select(const Call& c, cudaStream_t s);
 cudaError_t launch_compact(const Call& c, cudaStream_t s);
+cudaError_t launch_redundancy(const Call& c, cudaStream_t s);
 
 // ---- device helpers ----
 __device__ __forceinline__ float ex2f(float x) {

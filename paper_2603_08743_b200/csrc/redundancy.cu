@@ -1,0 +1,193 @@
+// NEXT-1: lightning redundancy score (§C.7), per unit (r, l, h) and block of b
+// tokens: C = cosine similarity of the block's key rows; C[i][i] = 0; per column j the LAST row i
+// (newest token) with C[i][j] > p is zeroed ("we prioritize retaining newer tokens");
+// r[t] = (row sum of C) / T. The softmax over the sequence with temperature tau and the combine
+// S - lambda*R happen in k_select. Slots >= T take no part (R20); a zero-norm
+// key has cosine 0 (R23); "above" is strictly greater (R21).
+//
+// k_red_mma (bf16, b = 16): one warp per block. The 16 rows are staged in shared memory (row stride
+// padded by 16 B so ldmatrix is conflict-free) and the 16 x 16 Gram matrix is 2 x d/16
+// mma.sync.m16n8k16 (bf16 -> fp32): one ldmatrix.x4 per K-step yields the A fragment and, because
+// B is the block's own rows, both B fragments (n-tile 0 = {a0, a2}, n-tile 1 = {a1, a3}).
+// k_red_generic (any dtype, b <= 32): one lane per row, fp32 dot products from L1; small/test shapes.
+#include "internal.h"
+
+namespace zpc {
+namespace {
+
+constexpr int kWarps = 8;            // warps per CTA (k_red_mma)
+constexpr int kBlocksPerWarp = 4;    // consecutive blocks per warp
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& a0, uint32_t& a1, uint32_t& a2, uint32_t& a3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void mma_bf16(float* c, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                         uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+      "{%0, %1, %2, %3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+template <int D>
+__global__ void __launch_bounds__(kWarps * 32) k_red_mma(Call c) {
+  if (*c.status != ZPC_OK) return;
+  constexpr int ROWB = D * 2 + 16;                 // padded row stride in shared memory (bytes)
+  __shared__ __align__(16) uint8_t stage[kWarps][16 * ROWB];
+  __shared__ float inv_norm[kWarps][16];
+  const int unit = blockIdx.x;
+  const int h = unit % c.h_kv;
+  const int l = (unit / c.h_kv) % c.L;
+  const int r = unit / (c.h_kv * c.L);
+  const int T = c.seq_lens[r];
+  const int nb = (T + 15) / 16;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int32_t* table = c.tables + (size_t)r * c.table_stride;
+  const uint16_t* K = reinterpret_cast<const uint16_t*>(c.k_cache);
+  float* out = c.ws.redund + (size_t)unit * c.max_seq_len;
+  const float inv_T = 1.0f / (float)T;
+  const float p = c.red_p;
+  uint8_t* st = stage[warp];
+  const uint32_t st_s = (uint32_t)__cvta_generic_to_shared(st);
+  const int r1 = lane >> 2, r2 = r1 + 8, cq = lane & 3;
+  const int cols[4] = {2 * cq, 2 * cq + 1, 8 + 2 * cq, 9 + 2 * cq};
+
+  for (int k = 0; k < kBlocksPerWarp; ++k) {
+    const int jb = (blockIdx.y * kWarps + warp) * kBlocksPerWarp + k;
+    if (jb >= nb) break;
+    const int j0 = jb * 16;
+    const int nvalid = min(16, T - j0);
+    const int blk = table[jb];
+    // stage the 16 rows (16-B vectors, coalesced along d); rows >= nvalid are loaded but masked
+    constexpr int CPR = D / 8;                      // 16-B chunks per row
+#pragma unroll
+    for (int q = lane; q < 16 * CPR; q += 32) {
+      const int row = q / CPR, ch = q % CPR;
+      const int4 v = *reinterpret_cast<const int4*>(K + kv_row(c, l, blk, row, h) + ch * 8);
+      *reinterpret_cast<int4*>(st + row * ROWB + ch * 16) = v;
+    }
+    __syncwarp();
+    // Gram matrix G = K_blk K_blk^T (16 x 16, fp32), two n-tiles of 8 columns
+    float g0[4] = {0.f, 0.f, 0.f, 0.f}, g1[4] = {0.f, 0.f, 0.f, 0.f};
+    const uint32_t a_addr = st_s + (uint32_t)((lane & 15) * ROWB + (lane >> 4) * 16);
+#pragma unroll
+    for (int s = 0; s < D / 16; ++s) {
+      uint32_t a0, a1, a2, a3;
+      ldsm_x4(a_addr + s * 32, a0, a1, a2, a3);
+      mma_bf16(g0, a0, a1, a2, a3, a0, a2);        // columns 0..7  (tokens 0..7)
+      mma_bf16(g1, a0, a1, a2, a3, a1, a3);        // columns 8..15 (tokens 8..15)
+    }
+    // this thread: G[r1][cols[0..3]] = g0[0], g0[1], g1[0], g1[1]; G[r2][...] = g0[2], g0[3], g1[2], g1[3]
+    float v1[4] = {g0[0], g0[1], g1[0], g1[1]}, v2[4] = {g0[2], g0[3], g1[2], g1[3]};
+    // squared norms from the diagonal -> 1/norm (0 for a zero-norm key or an invalid slot)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if (cols[e] == r1) inv_norm[warp][r1] = (v1[e] > 0.f && r1 < nvalid) ? 1.0f / sqrtf(v1[e]) : 0.f;
+      if (cols[e] == r2) inv_norm[warp][r2] = (v2[e] > 0.f && r2 < nvalid) ? 1.0f / sqrtf(v2[e]) : 0.f;
+    }
+    __syncwarp();
+    const float n1 = inv_norm[warp][r1], n2 = inv_norm[warp][r2];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float nc = inv_norm[warp][cols[e]];
+      v1[e] = (cols[e] == r1) ? 0.f : v1[e] * n1 * nc;   // invalid rows/cols carry a 0 norm
+      v2[e] = (cols[e] == r2) ? 0.f : v2[e] * n2 * nc;
+      // the column's last (largest row index) entry above p: rows of this column are spread over
+      // the 8 threads with the same lane & 3 (each holds rows r1 and r2 = r1 + 8)
+      int cand = v2[e] > p ? r2 : (v1[e] > p ? r1 : -1);
+      cand = max(cand, __shfl_xor_sync(0xffffffffu, cand, 4));
+      cand = max(cand, __shfl_xor_sync(0xffffffffu, cand, 8));
+      cand = max(cand, __shfl_xor_sync(0xffffffffu, cand, 16));
+      if (cand == r1) v1[e] = 0.f;
+      if (cand == r2) v2[e] = 0.f;
+    }
+    float s1 = (v1[0] + v1[1]) + (v1[2] + v1[3]);
+    float s2 = (v2[0] + v2[1]) + (v2[2] + v2[3]);
+    s1 += __shfl_xor_sync(0xffffffffu, s1, 1);
+    s1 += __shfl_xor_sync(0xffffffffu, s1, 2);
+    s2 += __shfl_xor_sync(0xffffffffu, s2, 1);
+    s2 += __shfl_xor_sync(0xffffffffu, s2, 2);
+    if (cq == 0) {
+      if (r1 < nvalid) out[j0 + r1] = s1 * inv_T;
+      if (r2 < nvalid) out[j0 + r2] = s2 * inv_T;
+    }
+    __syncwarp();   // the stage and inv_norm are rewritten for the next block
+  }
+}
+
+// any dtype, b <= 32: lane i owns row i of the block
+__global__ void __launch_bounds__(kWarps * 32) k_red_generic(Call c) {
+  if (*c.status != ZPC_OK) return;
+  const int unit = blockIdx.x;
+  const int h = unit % c.h_kv;
+  const int l = (unit / c.h_kv) % c.L;
+  const int r = unit / (c.h_kv * c.L);
+  const int T = c.seq_lens[r];
+  const int b = c.b;
+  const int nb = (T + b - 1) / b;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int32_t* table = c.tables + (size_t)r * c.table_stride;
+  float* out = c.ws.redund + (size_t)unit * c.max_seq_len;
+  const float inv_T = 1.0f / (float)T;
+  for (int jb = blockIdx.y * kWarps + warp; jb < nb; jb += gridDim.y * kWarps) {
+    const int j0 = jb * b;
+    const int nvalid = min(b, T - j0);
+    const int blk = table[jb];
+    const bool mine = lane < nvalid;
+    auto elem = [&](int row, int e) -> float {
+      const size_t off = kv_row(c, l, blk, row, h) + e;
+      return c.dtype == ZPC_BF16 ? bf16_to_f32(reinterpret_cast<const uint16_t*>(c.k_cache)[off])
+                                 : reinterpret_cast<const float*>(c.k_cache)[off];
+    };
+    float dots[32];
+    float nrm2 = 0.f;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) dots[j] = 0.f;
+    if (mine) {
+      for (int e = 0; e < c.d; ++e) {
+        const float ki = elem(lane, e);
+        nrm2 = fmaf(ki, ki, nrm2);
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (j < nvalid) dots[j] = fmaf(ki, elem(j, e), dots[j]);
+      }
+    }
+    const float inv_n = (mine && nrm2 > 0.f) ? 1.0f / sqrtf(nrm2) : 0.f;
+    float sum = 0.f;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      if (j >= b) break;
+      const float inv_nj = __shfl_sync(0xffffffffu, inv_n, j);
+      float cij = (mine && j < nvalid && j != lane) ? dots[j] * inv_n * inv_nj : 0.f;
+      int cand = cij > c.red_p ? lane : -1;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) cand = max(cand, __shfl_xor_sync(0xffffffffu, cand, o));
+      if (cand == lane) cij = 0.f;
+      sum += cij;
+    }
+    if (mine) out[j0 + lane] = sum * inv_T;
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_redundancy(const Call& c, cudaStream_t s) {
+  const int units = c.R * c.L * c.h_kv;
+  if (units == 0) return cudaSuccess;
+  if (c.dtype == ZPC_BF16 && c.b == 16) {
+    const int nb_max = (c.max_seq_len + 15) / 16;
+    const dim3 grid(units, (nb_max + kWarps * kBlocksPerWarp - 1) / (kWarps * kBlocksPerWarp));
+    if (c.d == 128) k_red_mma<128><<<grid, kWarps * 32, 0, s>>>(c);
+    else k_red_mma<64><<<grid, kWarps * 32, 0, s>>>(c);
+  } else {
+    const int nb_max = (c.max_seq_len + c.b - 1) / c.b;
+    const dim3 grid(units, min(64, (nb_max + kWarps - 1) / kWarps));
+    k_red_generic<<<grid, kWarps * 32, 0, s>>>(c);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace zpc

@@ -45,11 +45,37 @@ __device__ int block_excl(int v, int* sm, int* total) {
   return off;
 }
 
+__device__ float block_max(float v, float* sm) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if (lane == 0) sm[warp] = v;
+  __syncthreads();
+  float x = lane < kWarps ? sm[lane] : -INFINITY;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) x = fmaxf(x, __shfl_xor_sync(0xffffffffu, x, o));
+  __syncthreads();
+  return x;
+}
+__device__ float block_sum(float v, float* sm) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane == 0) sm[warp] = v;
+  __syncthreads();
+  float x = lane < kWarps ? sm[lane] : 0.f;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  __syncthreads();
+  return x;
+}
+
 __global__ void __launch_bounds__(kThreads) k_select(Call c) {
   if (*c.status != ZPC_OK) return;
   extern __shared__ uint32_t keys[];            // [T]
   __shared__ int hist[256];
   __shared__ int sm[kWarps];
+  __shared__ float fsm[kWarps];
   __shared__ uint32_t s_prefix;
   __shared__ int s_need;
 
@@ -63,7 +89,21 @@ __global__ void __launch_bounds__(kThreads) k_select(Call c) {
   const float* S = c.ws.scores + (size_t)unit * c.max_seq_len;
   const int half = c.pool_kernel / 2;
 
-  // load + pool + pin -> keys
+  // NEXT-1 (ZPC_F_REDUNDANCY): R = softmax(r / tau) over the sequence; the pooled
+  // score becomes S - lambda * R before the pin (R22)
+  const bool red = (c.flags & ZPC_F_REDUNDANCY) != 0;
+  const float* rr = c.ws.redund + (size_t)unit * c.max_seq_len;
+  float rmax = 0.f, rscale = 0.f;
+  const float inv_tau = red ? 1.0f / c.red_tau : 0.f;
+  if (red) {
+    float m = -INFINITY;
+    for (int t = threadIdx.x; t < T; t += kThreads) m = fmaxf(m, rr[t]);
+    rmax = block_max(m, fsm);
+    float z = 0.f;
+    for (int t = threadIdx.x; t < T; t += kThreads) z += expf((rr[t] - rmax) * inv_tau);
+    rscale = c.red_lambda / block_sum(z, fsm);      // lambda / sum
+  }
+  // load + pool (+ redundancy) + pin -> keys
   for (int t = threadIdx.x; t < T; t += kThreads) {
     float v;
     if (t >= T - c.w) {
@@ -72,6 +112,7 @@ __global__ void __launch_bounds__(kThreads) k_select(Call c) {
       v = S[t];
       const int lo = max(0, t - half), hi = min(T - 1, t + half);
       for (int j = lo; j <= hi; ++j) v = fmaxf(v, S[j]);
+      if (red) v -= rscale * expf((rr[t] - rmax) * inv_tau);
     }
     keys[t] = orderable(v);
   }

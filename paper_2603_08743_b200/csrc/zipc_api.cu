@@ -1,6 +1,7 @@
 // Host side of the C ABI (include/zipc.h): argument validation, workspace carving, stage
 // orchestration on the caller's stream, and the host-buffer e2e variant. No allocation, no
 // global state, no stream synchronisation.
+#include <cmath>
 #include <cstring>
 
 #include "internal.h"
@@ -24,6 +25,12 @@ bool desc_ok(const zpc_cache_desc* d, const zpc_params* p) {
   if (p->pool_kernel < 1 || (p->pool_kernel % 2) == 0) return false;
   if (p->max_seq_len < 1 || p->max_seq_len > ZPC_MAX_SEQ_LEN) return false;
   if ((long long)(p->n_max - 1) * d->block_size > (1LL << 30)) return false;
+  if (p->flags & ZPC_F_REDUNDANCY) {
+    if (!std::isfinite(p->redundancy_lambda) || !std::isfinite(p->redundancy_tau) || !std::isfinite(p->redundancy_p)) return false;
+    if (p->redundancy_lambda < 0.f || p->redundancy_tau <= 0.f) return false;
+    if (p->redundancy_p < 0.f || p->redundancy_p > 1.f) return false;
+    if (d->block_size > 32) return false;   // one warp per block
+  }
   return true;
 }
 
@@ -47,6 +54,7 @@ bool compute_layout(const zpc_cache_desc* d, const zpc_params* p, int32_t R, Lay
   o->pub.n_prefix = take((size_t)R * sizeof(int32_t));
   o->pub.lse = take(units * G * d->window * sizeof(float));
   o->pub.moves = take(sizeof(unsigned long long));
+  o->pub.redundancy = take((p->flags & ZPC_F_REDUNDANCY) ? units * p->max_seq_len * sizeof(float) : 0);
   o->pub.internal = off;
   o->req_err = take((size_t)R * sizeof(int32_t));
   o->n_blocks = take((size_t)R * sizeof(int32_t));
@@ -97,6 +105,8 @@ int make_call(const zpc_cache_desc* d, const zpc_params* p, const zpc_batch* b, 
   c->ws.n_prefix = reinterpret_cast<int32_t*>(w + ls.pub.n_prefix);
   c->ws.lse = reinterpret_cast<float*>(w + ls.pub.lse);
   c->ws.moves = reinterpret_cast<unsigned long long*>(w + ls.pub.moves);
+  c->ws.redund = reinterpret_cast<float*>(w + ls.pub.redundancy);
+  c->red_lambda = p->redundancy_lambda; c->red_tau = p->redundancy_tau; c->red_p = p->redundancy_p;
   c->ws.req_err = reinterpret_cast<int32_t*>(w + ls.req_err);
   c->ws.n_blocks = reinterpret_cast<int32_t*>(w + ls.n_blocks);
   c->ws.fresh_off = reinterpret_cast<int32_t*>(w + ls.fresh_off);
@@ -154,6 +164,10 @@ ZPC_STAGE(zpc_plan, {
   return cuda_rc(launch_plan(c, s));
 })
 ZPC_STAGE(zpc_score, { return run_score(c, s); })
+ZPC_STAGE(zpc_redundancy, {
+  if (!(c.flags & ZPC_F_REDUNDANCY)) return ZPC_OK;
+  return cuda_rc(launch_redundancy(c, s));
+})
 ZPC_STAGE(zpc_select, { return cuda_rc(launch_select(c, s)); })
 ZPC_STAGE(zpc_compact, { return cuda_rc(launch_compact(c, s)); })
 ZPC_STAGE(zpc_finalize, { return cuda_rc(launch_finalize(c, s)); })
@@ -161,6 +175,7 @@ ZPC_STAGE(zpc_compress, {
   if (c.flags & ZPC_F_COUNT_MOVES) cudaMemsetAsync(c.ws.moves, 0, sizeof(unsigned long long), s);
   if ((rc = cuda_rc(launch_plan(c, s))) != ZPC_OK) return rc;
   if ((rc = run_score(c, s)) != ZPC_OK) return rc;
+  if ((c.flags & ZPC_F_REDUNDANCY) && (rc = cuda_rc(launch_redundancy(c, s))) != ZPC_OK) return rc;
   if ((rc = cuda_rc(launch_select(c, s))) != ZPC_OK) return rc;
   if ((rc = cuda_rc(launch_compact(c, s))) != ZPC_OK) return rc;
   return cuda_rc(launch_finalize(c, s));

@@ -32,12 +32,13 @@ ZPC_F_PREFIX = 1
 ZPC_F_VALIDATE = 2
 ZPC_F_COUNT_MOVES = 4
 ZPC_F_SCORE_CUDACORE = 8
+ZPC_F_REDUNDANCY = 16
 
 ZPC_MAX_SEQ_LEN = 49152
 
 # exported symbols (the judge's / tests' export check compares with include/zipc.h)
 EXPORTS = ["zpc_workspace_bytes", "zpc_workspace_layout_get", "zpc_compress", "zpc_plan", "zpc_score",
-           "zpc_select", "zpc_compact", "zpc_finalize", "zpc_workspace_bytes_host", "zpc_compress_host",
+           "zpc_redundancy", "zpc_select", "zpc_compact", "zpc_finalize", "zpc_workspace_bytes_host", "zpc_compress_host",
            "zpc_status_string", "zpc_abi_version"]
 
 I32 = ctypes.c_int32
@@ -51,7 +52,9 @@ class zpc_cache_desc(ctypes.Structure):
 
 
 class zpc_params(ctypes.Structure):
-    _fields_ = [("n_max", I32), ("pool_kernel", I32), ("max_seq_len", I32), ("flags", ctypes.c_uint32)]
+    _fields_ = [("n_max", I32), ("pool_kernel", I32), ("max_seq_len", I32), ("flags", ctypes.c_uint32),
+                ("redundancy_lambda", ctypes.c_float), ("redundancy_tau", ctypes.c_float),
+                ("redundancy_p", ctypes.c_float)]
 
 
 class zpc_batch(ctypes.Structure):
@@ -66,8 +69,8 @@ class zpc_batch(ctypes.Structure):
 class zpc_workspace_layout(ctypes.Structure):
     _fields_ = [("total_bytes", ctypes.c_size_t), ("scores", ctypes.c_size_t), ("kept", ctypes.c_size_t),
                 ("targets", ctypes.c_size_t), ("reserved", ctypes.c_size_t), ("n_prefix", ctypes.c_size_t),
-                ("lse", ctypes.c_size_t), ("moves", ctypes.c_size_t), ("internal", ctypes.c_size_t),
-                ("kept_stride", I32)]
+                ("lse", ctypes.c_size_t), ("moves", ctypes.c_size_t), ("redundancy", ctypes.c_size_t),
+                ("internal", ctypes.c_size_t), ("kept_stride", I32)]
 
 
 class ZipcError(RuntimeError):
@@ -87,8 +90,8 @@ def lib() -> ctypes.CDLL:
             raise RuntimeError(f"{LIB_PATH} missing: run __graft_entry__.build() (no CPU fallback exists)")
         L = ctypes.CDLL(LIB_PATH)
         DP, PP, BP = ctypes.POINTER(zpc_cache_desc), ctypes.POINTER(zpc_params), ctypes.POINTER(zpc_batch)
-        for name in ("zpc_compress", "zpc_plan", "zpc_score", "zpc_select", "zpc_compact", "zpc_finalize",
-                     "zpc_compress_host"):
+        for name in ("zpc_compress", "zpc_plan", "zpc_score", "zpc_redundancy", "zpc_select", "zpc_compact",
+                     "zpc_finalize", "zpc_compress_host"):
             f = getattr(L, name)
             f.argtypes = [DP, PP, BP, P]
             f.restype = ctypes.c_int
@@ -114,8 +117,11 @@ def make_desc(L, h_kv, h_q, d, b, N_total, M, w, dtype) -> zpc_cache_desc:
     return zpc_cache_desc(L, h_kv, h_q, d, b, N_total, M, w, int(code))
 
 
-def make_params(n_max, pool_kernel=1, max_seq_len=ZPC_MAX_SEQ_LEN, flags=0) -> zpc_params:
-    return zpc_params(n_max, pool_kernel, max_seq_len, flags)
+def make_params(n_max, pool_kernel=1, max_seq_len=ZPC_MAX_SEQ_LEN, flags=0, redundancy_lambda=0.2,
+                redundancy_tau=0.4, redundancy_p=0.8) -> zpc_params:
+    """redundancy_*: used with ZPC_F_REDUNDANCY (PAPER.md:718 recommends lambda 0.2, tau 0.4; the paper
+    gives no value for p, 0.8 is a placeholder)."""
+    return zpc_params(n_max, pool_kernel, max_seq_len, flags, redundancy_lambda, redundancy_tau, redundancy_p)
 
 
 def zpc_workspace_bytes(desc, params, R) -> int:
@@ -180,6 +186,10 @@ def zpc_plan(desc, params, batch, stream=None, check=True):
 
 def zpc_score(desc, params, batch, stream=None, check=True):
     return _call("zpc_score", desc, params, batch, stream, check)
+
+
+def zpc_redundancy(desc, params, batch, stream=None, check=True):
+    return _call("zpc_redundancy", desc, params, batch, stream, check)
 
 
 def zpc_select(desc, params, batch, stream=None, check=True):

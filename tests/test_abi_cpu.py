@@ -25,7 +25,7 @@ def test_library_exports_every_declared_symbol():
     L = zipc.lib()
     for name in header_functions():
         assert hasattr(L, name), name
-    assert zipc.zpc_abi_version() == 1
+    assert zipc.zpc_abi_version() == 2
 
 
 def _desc(**kw):
@@ -40,8 +40,28 @@ def test_workspace_bytes_and_layout():
     lay = zipc.zpc_workspace_layout_get(_desc(), p, 64)
     assert n == lay.total_bytes > 64 * 28 * 4 * 8192 * 4
     assert lay.kept_stride == 128 * 16
-    offs = [lay.scores, lay.kept, lay.targets, lay.reserved, lay.n_prefix, lay.lse, lay.moves, lay.internal]
+    offs = [lay.scores, lay.kept, lay.targets, lay.reserved, lay.n_prefix, lay.lse, lay.moves, lay.redundancy,
+            lay.internal]
     assert offs == sorted(offs) and all(o % 256 == 0 for o in offs)
+    assert lay.internal == lay.redundancy            # zero-size region without ZPC_F_REDUNDANCY
+
+
+def test_redundancy_region_and_params():
+    """ZPC_F_REDUNDANCY adds an fp32 [R][L][h_kv][max_seq_len] region and validates lambda/tau/p."""
+    p0 = zipc.make_params(129, 7, 8192, 0)
+    p1 = zipc.make_params(129, 7, 8192, zipc.ZPC_F_REDUNDANCY)
+    lay0 = zipc.zpc_workspace_layout_get(_desc(), p0, 64)
+    lay1 = zipc.zpc_workspace_layout_get(_desc(), p1, 64)
+    assert lay1.internal - lay1.redundancy >= 64 * 28 * 4 * 8192 * 4
+    assert lay1.total_bytes - lay0.total_bytes >= 64 * 28 * 4 * 8192 * 4
+    for bad in (dict(redundancy_lambda=-0.1), dict(redundancy_tau=0.0), dict(redundancy_tau=-1.0),
+                dict(redundancy_p=1.5), dict(redundancy_p=-0.1), dict(redundancy_lambda=float("nan"))):
+        pb = zipc.make_params(129, 7, 8192, zipc.ZPC_F_REDUNDANCY, **bad)
+        assert zipc.zpc_workspace_bytes(_desc(), pb, 4) == 0, bad
+        # without the flag the same values are ignored
+        pn = zipc.make_params(129, 7, 8192, 0, **bad)
+        assert zipc.zpc_workspace_bytes(_desc(), pn, 4) > 0, bad
+    assert zipc.zpc_workspace_bytes(_desc(b=64), p1, 4) == 0   # one warp per block: b <= 32
 
 
 @pytest.mark.parametrize("bad", [dict(h_q=30), dict(d=96), dict(w=0), dict(dtype=7), dict(h_q=4 * 9, w=32)])
