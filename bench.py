@@ -108,7 +108,10 @@ def oracle_sample(cfg, seed, rids, n_req):
 _ORACLE_CACHE = {}
 
 
-def time_oracle(cfg, seed, n_req, budget_s=20.0):
+RED_PARAMS = (0.2, 0.4, 0.8)   # lambda, tau, p (NEXT-1)
+
+
+def time_oracle(cfg, seed, n_req, budget_s=20.0, redundancy=False):
     """Time the oracle (as it stands) on a bounded sample: whole requests restricted to a layer
     subset (the oracle's cost is per (layer, head) unit; req/s is scaled by units per request)."""
     import oracle as O
@@ -125,7 +128,8 @@ def time_oracle(cfg, seed, n_req, budget_s=20.0):
     geo = O.Geometry(L=sub.L, h_kv=sub.h_kv, h_q=sub.h_q, d=sub.d, b=sub.b, N_total=lay.N_total, M=lay.M,
                      w=sub.w, dtype=sub.dtype)
     prm = O.Params(n_max=sub.n_max, pool_kernel=sub.pool_kernel,
-                   flags=O.F_PREFIX if lay.ref_counts is not None else 0)
+                   flags=(O.F_PREFIX if lay.ref_counts is not None else 0) | (O.F_REDUNDANCY if redundancy else 0),
+                   lam=RED_PARAMS[0], tau=RED_PARAMS[1], sim_p=RED_PARAMS[2])
     units_done = 0
     t0 = time.perf_counter()
     while True:
@@ -195,6 +199,17 @@ def measured_traffic(cfg, per_gpu):
     return out
 
 
+def redundancy_roofline(cfg, seq_lens, world, red_ms, peaks):
+    """NEXT-1 stage: reads K once (T*d*e per unit) and writes r (4T per unit): HBM-bound."""
+    e = 2 if cfg.dtype == "bf16" else 4
+    T = np.asarray(seq_lens, np.int64)
+    byts = int((T * cfg.d * e + 4 * T).sum() * cfg.L * cfg.h_kv)
+    ach = byts / (red_ms / 1e3) / 1e9 if red_ms else None
+    return {"kernel": "k_red_mma" if (cfg.dtype == "bf16" and cfg.b == 16) else "k_red_generic", "bound": "hbm",
+            "achieved": ach, "peak": peaks["hbm"], "unit": "GB/s", "frac": ach / peaks["hbm"] if ach else None,
+            "algorithmic_bytes_per_launch": byts, "ms": red_ms}
+
+
 # ---------------------------------------------------------------- GPU arm
 def algorithmic_bytes(cfg, seq_lens, budgets, moves):
     """SURVEY §8(d) per-unit algorithmic bytes summed over the batch."""
@@ -220,6 +235,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cudacore", action="store_true", help="force the CUDA-core scoring kernel")
+    ap.add_argument("--redundancy", action="store_true",
+                    help="NEXT-1: lightning redundancy + temperature softmax in the selection score "
+                         "(lambda 0.2, tau 0.4 as PAPER.md:718 recommends; p 0.8, the paper gives none)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -231,7 +249,8 @@ def main():
     per_gpu = cfg.wave or cfg.R
     workload = (f"{cfg.name}: {per_gpu} req/GPU x {cfg.seq_lens[0]} tok, L={cfg.L} h_kv={cfg.h_kv} h_q={cfg.h_q} "
                 f"d={cfg.d} b={cfg.b} w={cfg.w} N_max={cfg.n_max} budget={cfg.budget} pool={cfg.pool_kernel}"
-                + (f" prefix={cfg.prefix_tokens}" if cfg.prefix_tokens else ""))
+                + (f" prefix={cfg.prefix_tokens}" if cfg.prefix_tokens else "")
+                + (" + NEXT-1 lightning redundancy (lambda=0.2 tau=0.4 p=0.8)" if args.redundancy else ""))
 
     if args.impl == "reference":
         if rank != 0:
@@ -239,9 +258,9 @@ def main():
         steps = []
         info = None
         for _ in range(args.warmup):
-            time_oracle(cfg, args.seed, 1, budget_s=0.5)
+            time_oracle(cfg, args.seed, 1, budget_s=0.5, redundancy=args.redundancy)
         for _ in range(args.steps):
-            v, info = time_oracle(cfg, args.seed, 1, budget_s=3.0)
+            v, info = time_oracle(cfg, args.seed, 1, budget_s=3.0, redundancy=args.redundancy)
             steps.append(v)
         value = float(np.mean(steps))
         line = {"impl": "reference", "metric": "requests_compressed_per_s", "value": value, "unit": "req/s",
@@ -271,7 +290,7 @@ def main():
     rids = shard_rids(rank, world, per_gpu, cfg.R)
     w = generate(cfg, args.seed, rids, device=dev)
     flags = zipc.ZPC_F_COUNT_MOVES | (zipc.ZPC_F_SCORE_CUDACORE if args.cudacore else 0)
-    desc, params = desc_params(w, flags=flags)
+    desc, params = desc_params(w, flags=flags, redundancy=RED_PARAMS if args.redundancy else None)
     batch = batch_of(w, desc, params)
     stream = torch.cuda.current_stream()
     lay = w.layout
@@ -295,6 +314,9 @@ def main():
 
     stages = [zipc.zpc_plan, zipc.zpc_score, zipc.zpc_select, zipc.zpc_compact, zipc.zpc_finalize]
     stage_names = ["plan", "score", "select", "compact", "finalize"]
+    if args.redundancy:   # NEXT-1 stage between score and select (still one zpc_compress call in e2e)
+        stages.insert(2, zipc.zpc_redundancy)
+        stage_names.insert(2, "redundancy")
 
     def step(evs):
         evs[0].record(stream)
@@ -341,8 +363,8 @@ def main():
 
     peaks = load_peaks()
     ab = algorithmic_bytes(cfg, lay.seq_lens, w.budgets_host, moves)
-    score_ms = stage_ms[1] / args.steps
-    compact_ms = stage_ms[3] / args.steps
+    score_ms = stage_ms[stage_names.index("score")] / args.steps
+    compact_ms = stage_ms[stage_names.index("compact")] / args.steps
     step_bytes = ab["score"] + ab["select"] + ab["compact"]
     traffic = measured_traffic(cfg, per_gpu)
     roofline = {"kernel": "score (a1+a2)", "bound": "hbm", "achieved": ab["score"] / (score_ms / 1e3) / 1e9,
@@ -359,6 +381,9 @@ def main():
                              "frac": (ab["compact"] / (compact_ms / 1e3) / 1e9) / peaks["hbm"] if compact_ms else None,
                              "traffic": traffic.get("compact"), "algorithmic_bytes_per_launch": ab["compact"]},
         "step_hbm_frac": step_bytes / (ms_per_step / 1e3) / 1e9 / peaks["hbm"],
+        **({"redundancy_roofline": redundancy_roofline(cfg, lay.seq_lens, world,
+                                                        stage_ms[stage_names.index("redundancy")] / args.steps,
+                                                        peaks)} if args.redundancy else {}),
         "kv_tokens_per_s": T_sum * world / (ms_per_step / 1e3),
         "wall_s_incl_restores": wall,
     }
@@ -410,12 +435,14 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v_cpu, info = time_oracle(cfg, args.seed, 1, budget_s=15.0)
+        v_cpu, info = time_oracle(cfg, args.seed, 1, budget_s=15.0, redundancy=args.redundancy)
         cpu = {"value": v_cpu, "unit": "req/s", "cores": info["threads"], "kind": "oracle",
                "sample": info["sample"], "cpu": cpu_model(), "seconds": info["seconds"]}
 
     score_kernels = 2 if (args.cudacore or cfg.dtype != "bf16") else 1   # k_lse_cc+k_final_cc | k_score_tc
     launches_per_step = 2 + score_kernels + 1 + 1 + 2   # plan(2) score select compact finalize(2)
+    if args.redundancy:
+        launches_per_step += 1                            # k_red_mma / k_red_generic
     if rank == 0:
         line = {"metric": "requests_compressed_per_s", "value": value, "unit": "req/s", "n_gpus": world,
                 "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_per_step,

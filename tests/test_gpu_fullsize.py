@@ -110,3 +110,71 @@ def test_sampled_units_vs_oracle(run7b, r, l, h):
     v_now = w.v[l][blk, slot, h].cpu().numpy().view(np.uint16)
     np.testing.assert_array_equal(k_now, kt[kept])
     np.testing.assert_array_equal(v_now, vt)
+
+
+# ---- NEXT-1 at full size: the bench's launch configuration with ZPC_F_REDUNDANCY
+RED = (0.2, 0.4, 0.8)
+
+
+@pytest.fixture(scope="module")
+def run7b_red():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    cfg = CONFIGS["qwen7b"]
+    w = generate(cfg, 2603, np.arange(cfg.R))
+    tables0 = w.layout.tables.copy()
+    desc, params = desc_params(w, flags=zipc.ZPC_F_COUNT_MOVES, redundancy=RED)
+    zipc.zpc_compress(desc, params, batch_of(w, desc, params))
+    torch.cuda.synchronize()
+    return cfg, w, desc, params, tables0
+
+
+def test_redundancy_structure_full(run7b_red):
+    cfg, w, desc, params, tables0 = run7b_red
+    assert int(w.status.item()) == 0
+    np.testing.assert_array_equal(w.new_lens.cpu().numpy(), np.minimum(8192, w.budgets_host))
+    lay = zipc.zpc_workspace_layout_get(desc, params, cfg.R)
+    units = cfg.R * cfg.L * cfg.h_kv
+    kept = workspace_view(w, desc, params, "kept", torch.int32, (units, lay.kept_stride))
+    ell = w.new_lens.reshape(-1)
+    last = torch.gather(kept, 1, (ell[:, None] - cfg.w + torch.arange(cfg.w, device=kept.device)[None, :]).long())
+    assert bool((last == torch.arange(8192 - cfg.w, 8192, device=kept.device)[None, :]).all())
+    r = workspace_view(w, desc, params, "redundancy", torch.float32, (units, w.max_seq_len))[:, :8192]
+    # each row sums at most b-1 cosines in [-1, 1], divided by T
+    assert bool(torch.isfinite(r).all()) and bool((r.abs() <= (cfg.b - 1) / 8192 * (1 + 1e-5)).all())
+
+
+@pytest.mark.parametrize("r,l,h", SAMPLES)
+def test_redundancy_sampled_units_vs_oracle(run7b_red, r, l, h):
+    cfg, w, desc, params, tables0 = run7b_red
+    T, seed = 8192, 2603
+    kt = k_rows(cfg, seed, r, l, h, np.arange(T), T)
+    keys = O.widen(kt, "bf16").astype(np.float64)
+    units = cfg.R * cfg.L * cfg.h_kv
+    u = (r * cfg.L + l) * cfg.h_kv + h
+    rr = workspace_view(w, desc, params, "redundancy", torch.float32, (units, w.max_seq_len))[u, :T].cpu().numpy()
+    ref = O.lightning_redundancy_raw(keys, cfg.b, RED[2])
+    # threshold decisions are discrete: compare the blocks whose cosines all keep 2e-5 from p
+    ok = np.ones(T, bool)
+    for j0 in range(0, T, cfg.b):
+        C = O.cosine_matrix(keys[j0:j0 + cfg.b])
+        if np.abs(C[~np.eye(cfg.b, dtype=bool)] - RED[2]).min() < 2e-5:
+            ok[j0:j0 + cfg.b] = False
+    assert ok.mean() > 0.9
+    np.testing.assert_allclose(rr[ok], ref[ok], rtol=1e-5, atol=4e-5 / T)
+    # kept band on the oracle's combined score (absolute band: S' may cross zero)
+    q = q_rows(cfg, seed, r, l)
+    geo = O.Geometry(L=1, h_kv=1, h_q=cfg.G, d=cfg.d, b=cfg.b, N_total=T // cfg.b, M=1, w=cfg.w, dtype="bf16")
+    kf = O.widen(kt, "bf16").reshape(T // cfg.b, cfg.b, 1, cfg.d)
+    qf = O.widen(q[:, h * cfg.G:(h + 1) * cfg.G, :], "bf16")
+    pooled = O.max_pool(O.attention_scores(O.logits_dense(geo, qf, kf, np.arange(T // cfg.b), T, 0), T),
+                        cfg.pool_kernel)
+    s_ref = O.pin_window(O.combine_redundancy(pooled, ref, RED[0], RED[1]), T, cfg.w)
+    lay = zipc.zpc_workspace_layout_get(desc, params, cfg.R)
+    ell = int(w.new_lens[r, l, h].item())
+    kg = workspace_view(w, desc, params, "kept", torch.int32, (units, lay.kept_stride))[u, :ell].cpu().numpy()
+    band = 1e-3 * np.abs(pooled).max()
+    theta = np.sort(s_ref)[::-1][ell - 1]
+    kept = np.zeros(T, bool)
+    kept[kg] = True
+    assert np.all(kept[s_ref > theta + band]) and not np.any(kept[s_ref < theta - band])
