@@ -314,7 +314,7 @@ def main():
 
     stages = [zipc.zpc_plan, zipc.zpc_score, zipc.zpc_select, zipc.zpc_compact, zipc.zpc_finalize]
     stage_names = ["plan", "score", "select", "compact", "finalize"]
-    if args.redundancy:   # NEXT-1 stage between score and select (still one zpc_compress call in e2e)
+    if args.redundancy:   # NEXT-1 stage between score and select (zpc_compress runs it in that order)
         stages.insert(2, zipc.zpc_redundancy)
         stage_names.insert(2, "redundancy")
 

@@ -186,10 +186,11 @@ int zpc_compress(const zpc_cache_desc* desc, const zpc_params* params, const zpc
  * free stack and top, new_num_blocks. */
 int zpc_plan(const zpc_cache_desc* desc, const zpc_params* params, const zpc_batch* batch, void* stream);
 int zpc_score(const zpc_cache_desc* desc, const zpc_params* params, const zpc_batch* batch, void* stream);
-/* NEXT-1 stage (ZPC_F_REDUNDANCY): per unit and block of b tokens, the b x b cosine similarity of
- * the block's keys (diagonal zeroed, per column the last entry > p zeroed), row sums / T into the
- * workspace `redundancy` region; slots >= T take no part, a zero-norm key has cosine 0. A no-op
- * (returns ZPC_OK) when the flag is clear. zpc_select then folds lambda * softmax(r / tau) in. */
+/* NEXT-1 (ZPC_F_REDUNDANCY): per unit and block of b tokens, the b x b cosine similarity of the
+ * block's keys (diagonal zeroed, per column the last entry > p zeroed), row sums / T into the
+ * workspace `redundancy` region; slots >= T take no part, a zero-norm key has cosine 0.
+ * zpc_compress runs it between score and select; as a stage it is a no-op without the flag.
+ * zpc_select then folds lambda * softmax(r / tau) in. */
 int zpc_redundancy(const zpc_cache_desc* desc, const zpc_params* params, const zpc_batch* batch, void* stream);
 int zpc_select(const zpc_cache_desc* desc, const zpc_params* params, const zpc_batch* batch, void* stream);
 int zpc_compact(const zpc_cache_desc* desc, const zpc_params* params, const zpc_batch* batch, void* stream);

@@ -16,7 +16,8 @@ namespace zpc {
 namespace {
 
 constexpr int kWarps = 8;            // warps per CTA (k_red_mma)
-constexpr int kBlocksPerWarp = 4;    // consecutive blocks per warp
+constexpr int kBlocksPerWarp = 8;    // consecutive blocks per warp (the next block's rows are
+                                     // prefetched into registers while the current one is computed)
 
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& a0, uint32_t& a1, uint32_t& a2, uint32_t& a3) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
@@ -55,21 +56,32 @@ __global__ void __launch_bounds__(kWarps * 32) k_red_mma(Call c) {
   const int r1 = lane >> 2, r2 = r1 + 8, cq = lane & 3;
   const int cols[4] = {2 * cq, 2 * cq + 1, 8 + 2 * cq, 9 + 2 * cq};
 
+  constexpr int CPR = D / 8;                        // 16-B chunks per row
+  constexpr int NV = 16 * CPR / 32;                 // 16-B vectors per lane per block
+  const int jb_first = (blockIdx.y * kWarps + warp) * kBlocksPerWarp;
+  int4 pre[NV];
+  auto fetch = [&](int jb) {                        // this lane's share of block jb's 16 rows
+    const int blk = table[jb];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const int q = lane + 32 * v, row = q / CPR, ch = q % CPR;
+      pre[v] = *reinterpret_cast<const int4*>(K + kv_row(c, l, blk, row, h) + ch * 8);
+    }
+  };
+  if (jb_first < nb) fetch(jb_first);
   for (int k = 0; k < kBlocksPerWarp; ++k) {
-    const int jb = (blockIdx.y * kWarps + warp) * kBlocksPerWarp + k;
+    const int jb = jb_first + k;
     if (jb >= nb) break;
     const int j0 = jb * 16;
     const int nvalid = min(16, T - j0);
-    const int blk = table[jb];
-    // stage the 16 rows (16-B vectors, coalesced along d); rows >= nvalid are loaded but masked
-    constexpr int CPR = D / 8;                      // 16-B chunks per row
+    // stage block jb (rows >= nvalid are loaded but masked), then start fetching block jb + 1
 #pragma unroll
-    for (int q = lane; q < 16 * CPR; q += 32) {
-      const int row = q / CPR, ch = q % CPR;
-      const int4 v = *reinterpret_cast<const int4*>(K + kv_row(c, l, blk, row, h) + ch * 8);
-      *reinterpret_cast<int4*>(st + row * ROWB + ch * 16) = v;
+    for (int v = 0; v < NV; ++v) {
+      const int q = lane + 32 * v, row = q / CPR, ch = q % CPR;
+      *reinterpret_cast<int4*>(st + row * ROWB + ch * 16) = pre[v];
     }
     __syncwarp();
+    if (k + 1 < kBlocksPerWarp && jb + 1 < nb) fetch(jb + 1);
     // Gram matrix G = K_blk K_blk^T (16 x 16, fp32), two n-tiles of 8 columns
     float g0[4] = {0.f, 0.f, 0.f, 0.f}, g1[4] = {0.f, 0.f, 0.f, 0.f};
     const uint32_t a_addr = st_s + (uint32_t)((lane & 15) * ROWB + (lane >> 4) * 16);

@@ -167,3 +167,4 @@ def test_redundancy_flag_off_is_unchanged(cuda_ok):
         outs.append((to_host(w.new_lens), to_host(w.k, True), to_host(w.tables)))
     for a, b in zip(outs[0], outs[1]):
         np.testing.assert_array_equal(a, b)
+
