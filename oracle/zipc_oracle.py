@@ -36,6 +36,7 @@ ERR_CAPACITY = -16
 F_PREFIX = 1
 F_VALIDATE = 2
 F_REDUNDANCY = 16   # NEXT-1: lightning redundancy + temperature softmax + S - lambda*R
+F_GLOBAL_SCORE = 32  # NEXT-2: global score (Alg. 2) + F relocation with the kept rows
 
 
 @dataclass
@@ -65,6 +66,7 @@ class Params:
     lam: float = 0.2      # lambda, PAPER.md:718 (§C.8 recommended)
     tau: float = 0.4      # tau
     sim_p: float = 0.8    # similarity threshold p: no value in the paper (R19)
+    alpha: float = 0.8    # global-score decay, PAPER.md:718 (§C.8 recommended)
 
 
 # --------------------------------------------------------------------------
@@ -357,6 +359,41 @@ def unit_keys(geo: Geometry, k_pool_f64, table, T: int, l: int, h: int) -> np.nd
 
 
 # --------------------------------------------------------------------------
+# NEXT-2: global score — Alg. 2, PAPER.md:412-456 (§C.3), relocation PAPER.md:595 (§C.6)
+# Readings: R24 F is fp32 [L, N_total, b, h_kv]; R25 "not the last block of the
+# sequence" = the logical blocks i < N_max - 1 (the targets of the previous compaction; at the
+# paper's trigger N = N_max that is every block but the last); R26 the update uses S before pooling
+# and F keeps the updated, unpooled score; R27 an uncompressed request only stores S.
+# --------------------------------------------------------------------------
+def global_score_update(s: np.ndarray, f_layer: np.ndarray, table, T: int, h: int, b: int, n_max: int,
+                        compressed: bool, alpha: float) -> np.ndarray:
+    """Alg. 2 over the blocks of one unit, written out block by block. Mutates
+    f_layer ([N_total, b, h_kv] fp32) and returns the (possibly overwritten) scores."""
+    s = s.copy()
+    N = (T + b - 1) // b
+    for i in range(N):
+        lo, hi = i * b, min(T, (i + 1) * b)
+        si = s[lo:hi].copy()                                  # line 1: s_i of the i-th block
+        p = int(table[i])                                     # line 2: offset through the block table
+        if compressed and i < n_max - 1:                      # lines 6-8 (R25)
+            fi = f_layer[p, :hi - lo, h].astype(np.float64)
+            si = np.maximum(alpha * fi, si)
+        f_layer[p, :hi - lo, h] = si                          # lines 4 / 10 (fp32 store, R24)
+        if compressed:
+            s[lo:hi] = si                                     # line 11
+    return s
+
+
+def compact_gather_f(f_layer, table, targets, kept: np.ndarray, h: int, b: int):
+    """The global-score rows follow their K/V rows: new[rank] = old[kept[rank]]."""
+    table = np.asarray(table)
+    targets = np.asarray(targets)
+    fs = f_layer[table[kept // b], kept % b, h].copy()
+    rank = np.arange(len(kept))
+    f_layer[targets[rank // b], rank % b, h] = fs
+
+
+# --------------------------------------------------------------------------
 # a4: per-head top-l with the index tie rule — PAPER.md:85, :591 (§C.6)
 # --------------------------------------------------------------------------
 def select(s_final: np.ndarray, ell: int) -> np.ndarray:
@@ -483,12 +520,14 @@ class CompressOut:
     scores: dict = None              # (r, l, h) -> raw s (pre-pool) fp64
     fin: FinalizeOut = None
     redundancy: dict = None          # (r, l, h) -> lightning r_raw (pre-softmax) fp64 (F_REDUNDANCY)
+    f_cache: np.ndarray = None       # F after the step (F_GLOBAL_SCORE)
+    global_scores: dict = None       # (r, l, h) -> S after Alg. 2 (pre-pool) (F_GLOBAL_SCORE)
     plan: Plan = None
 
 
 def compress(geo: Geometry, prm: Params, k_cache, v_cache, q_cache, q_slots, seq_lens, tables, budgets,
              ref_counts=None, free_stack=None, free_top=0, kept_override=None, blockwise=False,
-             free_capacity=None, freed_capacity=None, units=None) -> CompressOut:
+             free_capacity=None, freed_capacity=None, units=None, f_cache=None, is_compressed=None) -> CompressOut:
     """Steps 1-9 of SURVEY.md §8(c) for every request r (input order), layer l, KV head h.
 
     kept_override: optional dict (r, l, h) -> kept list, used to drive compaction with
@@ -502,10 +541,12 @@ def compress(geo: Geometry, prm: Params, k_cache, v_cache, q_cache, q_slots, seq
     R = len(seq_lens)
     k_out = k_cache.copy()
     v_out = v_cache.copy()
+    use_global = bool(prm.flags & F_GLOBAL_SCORE)
+    f_out = f_cache.copy() if use_global else None
     qf = widen(q_cache, geo.dtype)
     kf = widen(k_cache, geo.dtype)
     new_lens = np.zeros((R, geo.L, geo.h_kv), np.int32)
-    kept_all, scores, redund = {}, {}, {}
+    kept_all, scores, redund, gscores = {}, {}, {}, {}
     for r in range(R):
         T = int(seq_lens[r])
         for l in range(geo.L):
@@ -520,6 +561,10 @@ def compress(geo: Geometry, prm: Params, k_cache, v_cache, q_cache, q_slots, seq
                         continue
                     s = unit_scores(geo, qf, kf, tables[r], T, int(q_slots[r]), l, h, blockwise)
                     scores[key] = s
+                    if use_global:
+                        s = global_score_update(s, f_out[l], tables[r], T, h, geo.b, prm.n_max,
+                                                bool(is_compressed[r]), prm.alpha)
+                        gscores[key] = s
                     sp = max_pool(s, prm.pool_kernel)
                     if prm.flags & F_REDUNDANCY:
                         rr = lightning_redundancy_raw(unit_keys(geo, kf, tables[r], T, l, h), geo.b, prm.sim_p)
@@ -535,6 +580,8 @@ def compress(geo: Geometry, prm: Params, k_cache, v_cache, q_cache, q_slots, seq
                 if key not in kept_all:
                     continue
                 compact_gather(k_out[l], v_out[l], tables[r], pl.targets[r], kept_all[key], h, geo.b)
+                if use_global:
+                    compact_gather_f(f_out[l], tables[r], pl.targets[r], kept_all[key], h, geo.b)
     fin = finalize(geo, prm, pl, tables, ref_counts, free_stack, free_top)
     return CompressOut(status=OK, k_cache=k_out, v_cache=v_out, new_lens=new_lens, kept=kept_all,
-                       scores=scores, fin=fin, plan=pl, redundancy=redund)
+                       scores=scores, fin=fin, plan=pl, redundancy=redund, f_cache=f_out, global_scores=gscores)
