@@ -52,7 +52,9 @@ extern "C" {
                                        unsupported head_dim/dtype, h_q not a multiple of h_kv,
                                        G*w > 256, max_seq_len above the select limit, NULL pointer,
                                        ZPC_F_REDUNDANCY with lambda < 0, tau <= 0, p outside [0,1],
-                                       a non-finite value or block_size > 32 */
+                                       a non-finite value or block_size > 32, ZPC_F_GLOBAL_SCORE
+                                       with alpha outside [0,1] or a NULL global_scores /
+                                       is_compressed */
 #define ZPC_ERR_WORKSPACE      -2   /* workspace_bytes < zpc_workspace_bytes(...) */
 #define ZPC_ERR_CUDA           -3   /* a launch failed (cudaGetLastError) */
 #define ZPC_ERR_NOT_TRIGGERED -10   /* device: N = ceil(T/b) < N_max */
@@ -82,6 +84,12 @@ extern "C" {
                                  temperature softmax (§C.8) folded into the selection
                                  score after pooling: S = MaxPool(S) - lambda * softmax(r / tau)
                                  (PAPER.md:506). Uses params.redundancy_*; adds a workspace region. */
+#define ZPC_F_GLOBAL_SCORE 32u /* NEXT-2: global score, Alg. 2 (§C.3): per block of a
+                                 request, F <- S when is_compressed[r] == 0; otherwise S <- max(alpha F,
+                                 S) on the logical blocks < N_max-1 (the previous targets), F <- S;
+                                 pooling etc. then use the updated S, and compaction moves each kept
+                                 row's F with its K/V. Needs batch.global_scores and
+                                 batch.is_compressed; params.global_alpha. */
 
 /* Pool geometry: K, V [L][N_total][b][h_kv][d], Q [L][M][w][h_q][d].
  * Q row u of slot j holds the query of position T-w+u of the request bound to slot j (R3). */
@@ -111,6 +119,8 @@ typedef struct {
   float redundancy_lambda;
   float redundancy_tau;
   float redundancy_p;
+  /* ZPC_F_GLOBAL_SCORE only: decay alpha in [0, 1] (PAPER.md:441; 0.8 recommended, :718) */
+  float global_alpha;
 } zpc_params;
 
 #define ZPC_MAX_SEQ_LEN 49152   /* select keeps a unit's scores in shared memory */
@@ -152,6 +162,11 @@ typedef struct {
   void* workspace;          /* device scratch, >= zpc_workspace_bytes(...), 256-B aligned */
   size_t workspace_bytes;
   int32_t* status;
+  /* ZPC_F_GLOBAL_SCORE only (else ignored, may be NULL):
+   *   global_scores  dev fp32 [L][N_total][b][h_kv], in/out: F, the global-score pool
+   *   is_compressed  dev int32 [R], 0 or 1: the request was compressed before (Alg. 2 line 3) */
+  float* global_scores;
+  const int32_t* is_compressed;
 } zpc_batch;
 
 /* Where intermediate results live inside the workspace (byte offsets; all 256-B aligned). */
@@ -181,8 +196,9 @@ int zpc_compress(const zpc_cache_desc* desc, const zpc_params* params, const zpc
 /* Stage entry points (same conventions; each consumes the previous stage's workspace output).
  * zpc_plan writes *status, targets/reserved/n_prefix and the internal scan; it mutates nothing
  * outside the workspace and *status. zpc_score writes S and LSE. zpc_select writes kept and
- * new_lens (with ZPC_F_REDUNDANCY it reads the `redundancy` region written by zpc_redundancy).
- * zpc_compact moves K/V rows. zpc_finalize rewrites tables, ref counts, freed list,
+ * new_lens (with ZPC_F_REDUNDANCY it reads the `redundancy` region written by zpc_redundancy; with
+ * ZPC_F_GLOBAL_SCORE it applies Alg. 2 first: updates F and overwrites S with the global score).
+ * zpc_compact moves K/V rows (and F rows with ZPC_F_GLOBAL_SCORE). zpc_finalize rewrites tables, ref counts, freed list,
  * free stack and top, new_num_blocks. */
 int zpc_plan(const zpc_cache_desc* desc, const zpc_params* params, const zpc_batch* batch, void* stream);
 int zpc_score(const zpc_cache_desc* desc, const zpc_params* params, const zpc_batch* batch, void* stream);
@@ -198,8 +214,9 @@ int zpc_finalize(const zpc_cache_desc* desc, const zpc_params* params, const zpc
 
 /* End-to-end variant for host-resident bookkeeping (the e2e benchmark path): `host` holds the
  * same fields, but q_slots, seq_lens, block_tables, budgets, new_lens, new_num_blocks,
- * ref_counts, free_stack, free_top, freed_blocks, num_freed and status point to HOST memory
- * (pinned for async copies); k_cache, v_cache, q_cache and workspace are device memory.
+ * ref_counts, free_stack, free_top, freed_blocks, num_freed, status and is_compressed point to HOST
+ * memory (pinned for async copies); k_cache, v_cache, q_cache, global_scores and workspace are
+ * device memory.
  * The call stages the host inputs into the workspace (H2D), runs zpc_compress, and copies every
  * output back (D2H), all on `stream`. Host buffers must stay alive until the stream is synced.
  * Workspace must be >= zpc_workspace_bytes_host(...). */

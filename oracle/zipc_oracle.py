@@ -556,6 +556,10 @@ def compress(geo: Geometry, prm: Params, k_cache, v_cache, q_cache, q_slots, seq
                 key = (r, l, h)
                 if kept_override is not None and key in kept_override:
                     kept = np.asarray(kept_override[key], np.int32)
+                    if use_global:   # F is still updated by Alg. 2 before it is relocated
+                        s = unit_scores(geo, qf, kf, tables[r], T, int(q_slots[r]), l, h, blockwise)
+                        gscores[key] = global_score_update(s, f_out[l], tables[r], T, h, geo.b, prm.n_max,
+                                                           bool(is_compressed[r]), prm.alpha)
                 else:
                     if units is not None and key not in units:
                         continue

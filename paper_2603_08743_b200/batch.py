@@ -11,16 +11,20 @@ import torch
 from . import zipc
 
 
-def desc_params(w, flags=0, pool_kernel=None, max_seq_len=None, redundancy=None):
-    """redundancy: None, or (lambda, tau, p) -> sets ZPC_F_REDUNDANCY with those parameters."""
+def desc_params(w, flags=0, pool_kernel=None, max_seq_len=None, redundancy=None, global_alpha=None):
+    """redundancy: None, or (lambda, tau, p) -> sets ZPC_F_REDUNDANCY with those parameters.
+    global_alpha: None, or alpha -> sets ZPC_F_GLOBAL_SCORE (w.f_cache / w.is_compressed must exist)."""
     cfg, lay = w.cfg, w.layout
     desc = zipc.make_desc(cfg.L, cfg.h_kv, cfg.h_q, cfg.d, cfg.b, lay.N_total, lay.M, cfg.w, cfg.dtype)
     if w.ref_counts is not None:
         flags |= zipc.ZPC_F_PREFIX
     extra = {}
+    if global_alpha is not None:
+        flags |= zipc.ZPC_F_GLOBAL_SCORE
+        extra["global_alpha"] = global_alpha
     if redundancy is not None:
         flags |= zipc.ZPC_F_REDUNDANCY
-        extra = dict(redundancy_lambda=redundancy[0], redundancy_tau=redundancy[1], redundancy_p=redundancy[2])
+        extra.update(redundancy_lambda=redundancy[0], redundancy_tau=redundancy[1], redundancy_p=redundancy[2])
     params = zipc.make_params(cfg.n_max, cfg.pool_kernel if pool_kernel is None else pool_kernel,
                               int(max_seq_len or w.max_seq_len), flags, **extra)
     return desc, params
@@ -41,7 +45,8 @@ def batch_of(w, desc, params):
                            block_tables=w.tables, budgets=w.budgets, new_lens=w.new_lens,
                            new_num_blocks=w.new_num_blocks, ref_counts=w.ref_counts, free_stack=w.free_stack,
                            free_top=w.free_top, freed_blocks=w.freed, num_freed=w.num_freed,
-                           workspace=w.workspace, status=w.status)
+                           workspace=w.workspace, status=w.status,
+                           global_scores=getattr(w, "f_cache", None), is_compressed=getattr(w, "is_compressed", None))
 
 
 def workspace_view(w, desc, params, name, dtype, shape):

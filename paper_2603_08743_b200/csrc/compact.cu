@@ -23,12 +23,14 @@ template <int VPR, int kVec>
 struct Chunk {
   int4 k[kVec], v[kVec];
   uint32_t dst[kVec];                // destination vector index within the layer-head plane, ~0u = none
+  float f[kVec];                     // NEXT-2: the row's global score (the row's first vector carries it)
+  uint32_t fdst[kVec];               // its destination row (blk*b + slot), ~0u = none
 };
 
 template <int VPR, int kVec>
 __device__ __forceinline__ void load_chunk(const Call& c, Chunk<VPR, kVec>& ch, int base, int ell, const int32_t* kept,
                                            const int32_t* table, const int32_t* tg, const int4* K, const int4* V,
-                                           size_t plane, int bsh) {
+                                           size_t plane, int bsh, const float* F, size_t fplane) {
   constexpr int CH = kVec * kThreads / VPR;        // ranks per chunk
   const int nvec = min(CH, ell - base) * VPR;
   const uint32_t rowv = (uint32_t)c.h_kv * VPR;    // vectors between consecutive slots
@@ -50,10 +52,15 @@ __device__ __forceinline__ void load_chunk(const Call& c, Chunk<VPR, kVec>& ch, 
       // vector index relative to the (layer, head) plane: (blk*b + slot)*h_kv*VPR + e
       const uint32_t src = ((uint32_t)sblk * c.b + sslot) * rowv + e;
       const uint32_t d = ((uint32_t)dblk * c.b + dslot) * rowv + e;
+      ch.fdst[k] = ~0u;
       if (src != d) {
         ch.k[k] = K[plane + src];
         ch.v[k] = V[plane + src];
         ch.dst[k] = d;
+        if (F && e == 0) {            // F moves with its K/V row
+          ch.f[k] = F[fplane + ((size_t)sblk * c.b + sslot) * c.h_kv];
+          ch.fdst[k] = (uint32_t)dblk * c.b + dslot;
+        }
       }
     }
   }
@@ -79,19 +86,22 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_compact(Call c) {
   int4* Vw = reinterpret_cast<int4*>(c.v_cache);
   // start of the (layer l, head h) plane in vectors; per-row offsets are 32-bit within a layer
   const size_t plane = (size_t)l * c.N_total * c.b * c.h_kv * VPR + (size_t)h * VPR;
+  float* Fw = (c.flags & ZPC_F_GLOBAL_SCORE) ? c.f_cache : nullptr;   // NEXT-2 relocation
+  const size_t fplane = (size_t)l * c.N_total * c.b * c.h_kv + h;
   unsigned moved = 0;
 
   Chunk<VPR, kVec> cur, nxt;
-  if (ell > 0) load_chunk<VPR, kVec>(c, cur, 0, ell, kept, table, tg, K, V, plane, bsh);
+  if (ell > 0) load_chunk<VPR, kVec>(c, cur, 0, ell, kept, table, tg, K, V, plane, bsh, Fw, fplane);
   for (int base = 0; base < ell; base += CH) {
     __syncthreads();   // every read of chunk `base` has returned before any write of it
     const bool more = base + CH < ell;
-    if (more) load_chunk<VPR, kVec>(c, nxt, base + CH, ell, kept, table, tg, K, V, plane, bsh);
+    if (more) load_chunk<VPR, kVec>(c, nxt, base + CH, ell, kept, table, tg, K, V, plane, bsh, Fw, fplane);
 #pragma unroll
     for (int k = 0; k < kVec; ++k) {
       if (cur.dst[k] != ~0u) {
         Kw[plane + cur.dst[k]] = cur.k[k];
         Vw[plane + cur.dst[k]] = cur.v[k];
+        if (cur.fdst[k] != ~0u) Fw[fplane + (size_t)cur.fdst[k] * c.h_kv] = cur.f[k];
         moved += ((threadIdx.x + k * kThreads) % VPR) == 0;
       }
     }

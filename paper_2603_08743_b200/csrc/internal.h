@@ -33,6 +33,7 @@ struct Call {
   uint32_t flags;
   uint32_t debug;      // tuning/bisection switches (ZPC_SCORE_DEBUG), 0 in production
   float red_lambda, red_tau, red_p;   // ZPC_F_REDUNDANCY parameters
+  float global_alpha;                 // ZPC_F_GLOBAL_SCORE decay
   int32_t R, table_stride, free_capacity, freed_capacity;
   void* k_cache;
   void* v_cache;
@@ -49,6 +50,8 @@ struct Call {
   int32_t* freed;
   int32_t* num_freed;
   int32_t* status;
+  float* f_cache;                     // ZPC_F_GLOBAL_SCORE: F [L][N_total][b][h_kv]
+  const int32_t* is_compressed;       // ZPC_F_GLOBAL_SCORE: [R]
   Ws ws;
 };
 

@@ -89,6 +89,24 @@ __global__ void __launch_bounds__(kThreads) k_select(Call c) {
   const float* S = c.ws.scores + (size_t)unit * c.max_seq_len;
   const int half = c.pool_kernel / 2;
 
+  // NEXT-2 (ZPC_F_GLOBAL_SCORE): Alg. 2 over the unit's blocks before pooling
+  // (PAPER.md:487): F <- S for a request never compressed; otherwise S <- max(alpha F, S) on the
+  // logical blocks < N_max-1 (the previous targets, R25), F <- S, and S is overwritten (line 11)
+  if (c.flags & ZPC_F_GLOBAL_SCORE) {
+    const bool comp = c.is_compressed[r] != 0;
+    const int32_t* table = c.tables + (size_t)r * c.table_stride;
+    float* Sw = c.ws.scores + (size_t)unit * c.max_seq_len;
+    const size_t fplane = (size_t)l * c.N_total * c.b * c.h_kv + h;
+    for (int t = threadIdx.x; t < T; t += kThreads) {
+      const int i = t / c.b;
+      float* fp = c.f_cache + fplane + ((size_t)table[i] * c.b + (t - i * c.b)) * c.h_kv;
+      float v = Sw[t];
+      if (comp && i < c.n_max - 1) v = fmaxf(c.global_alpha * *fp, v);
+      *fp = v;
+      if (comp) Sw[t] = v;
+    }
+    __syncthreads();
+  }
   // NEXT-1 (ZPC_F_REDUNDANCY): R = softmax(r / tau) over the sequence; the pooled
   // score becomes S - lambda * R before the pin (R22)
   const bool red = (c.flags & ZPC_F_REDUNDANCY) != 0;

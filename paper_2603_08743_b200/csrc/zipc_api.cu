@@ -31,6 +31,9 @@ bool desc_ok(const zpc_cache_desc* d, const zpc_params* p) {
     if (p->redundancy_p < 0.f || p->redundancy_p > 1.f) return false;
     if (d->block_size > 32) return false;   // one warp per block
   }
+  if (p->flags & ZPC_F_GLOBAL_SCORE) {
+    if (!std::isfinite(p->global_alpha) || p->global_alpha < 0.f || p->global_alpha > 1.f) return false;
+  }
   return true;
 }
 
@@ -78,6 +81,7 @@ int make_call(const zpc_cache_desc* d, const zpc_params* p, const zpc_batch* b, 
   if (!b->free_stack || !b->free_top || !b->freed_blocks || !b->num_freed) return ZPC_ERR_INVALID_ARG;
   if (b->table_stride < 1 && b->num_requests > 0) return ZPC_ERR_INVALID_ARG;
   if ((p->flags & ZPC_F_PREFIX) && !b->ref_counts) return ZPC_ERR_INVALID_ARG;
+  if ((p->flags & ZPC_F_GLOBAL_SCORE) && (!b->global_scores || !b->is_compressed)) return ZPC_ERR_INVALID_ARG;
   if ((reinterpret_cast<uintptr_t>(b->workspace) & (kAlign - 1)) != 0) return ZPC_ERR_INVALID_ARG;
   if (b->workspace_bytes < ls.pub.total_bytes) return ZPC_ERR_WORKSPACE;
   const int esz = d->dtype == ZPC_BF16 ? 2 : 4;
@@ -107,6 +111,9 @@ int make_call(const zpc_cache_desc* d, const zpc_params* p, const zpc_batch* b, 
   c->ws.moves = reinterpret_cast<unsigned long long*>(w + ls.pub.moves);
   c->ws.redund = reinterpret_cast<float*>(w + ls.pub.redundancy);
   c->red_lambda = p->redundancy_lambda; c->red_tau = p->redundancy_tau; c->red_p = p->redundancy_p;
+  c->global_alpha = p->global_alpha;
+  c->f_cache = b->global_scores;
+  c->is_compressed = b->is_compressed;
   c->ws.req_err = reinterpret_cast<int32_t*>(w + ls.req_err);
   c->ws.n_blocks = reinterpret_cast<int32_t*>(w + ls.n_blocks);
   c->ws.fresh_off = reinterpret_cast<int32_t*>(w + ls.fresh_off);
@@ -188,7 +195,7 @@ size_t zpc_workspace_bytes_host(const zpc_cache_desc* d, const zpc_params* p, in
   const size_t units = (size_t)R * d->num_layers * d->num_kv_heads;
   size_t off = ls.pub.total_bytes;
   auto take = [&](size_t bytes) { off = align_up(off + bytes); };
-  take((size_t)R * sizeof(int32_t) * 3);                       // q_slots, seq_lens, new_num_blocks
+  take((size_t)R * sizeof(int32_t) * 4);                       // q_slots, seq_lens, new_num_blocks, is_compressed
   take((size_t)R * table_stride * sizeof(int32_t));             // tables
   take(units * sizeof(int32_t) * 2);                            // budgets, new_lens
   take((size_t)d->num_blocks * sizeof(int32_t));                // ref counts
@@ -210,9 +217,10 @@ int zpc_compress_host(const zpc_cache_desc* d, const zpc_params* p, const zpc_ba
   char* base = static_cast<char*>(h->workspace);
   size_t off = ls.pub.total_bytes;      // same carving order as zpc_workspace_bytes_host
   auto take = [&](size_t bytes) { char* at = base + off; off = align_up(off + bytes); return at; };
-  int32_t* q_slots = reinterpret_cast<int32_t*>(take((size_t)R * 12));
+  int32_t* q_slots = reinterpret_cast<int32_t*>(take((size_t)R * 16));
   int32_t* seq_lens = q_slots + R;
   int32_t* nnb = q_slots + 2 * R;
+  int32_t* comp = q_slots + 3 * R;
   int32_t* tables = reinterpret_cast<int32_t*>(take((size_t)R * h->table_stride * 4));
   int32_t* budgets = reinterpret_cast<int32_t*>(take(units * 8));
   int32_t* new_lens = budgets + units;
@@ -226,6 +234,8 @@ int zpc_compress_host(const zpc_cache_desc* d, const zpc_params* p, const zpc_ba
     cudaMemcpyAsync(seq_lens, h->seq_lens, (size_t)R * 4, H2D, s);
     cudaMemcpyAsync(tables, h->block_tables, (size_t)R * h->table_stride * 4, H2D, s);
     cudaMemcpyAsync(budgets, h->budgets, units * 4, H2D, s);
+    if ((p->flags & ZPC_F_GLOBAL_SCORE) && h->is_compressed)
+      cudaMemcpyAsync(comp, h->is_compressed, (size_t)R * 4, H2D, s);
   }
   if (h->ref_counts) cudaMemcpyAsync(refs, h->ref_counts, (size_t)d->num_blocks * 4, H2D, s);
   cudaMemcpyAsync(stack, h->free_stack, (size_t)h->free_capacity * 4, H2D, s);
@@ -235,6 +245,7 @@ int zpc_compress_host(const zpc_cache_desc* d, const zpc_params* p, const zpc_ba
   dv.new_lens = new_lens; dv.new_num_blocks = nnb; dv.ref_counts = h->ref_counts ? refs : nullptr;
   dv.free_stack = stack; dv.free_top = small; dv.freed_blocks = freed; dv.num_freed = small + 1;
   dv.status = small + 2; dv.workspace = h->workspace; dv.workspace_bytes = ls.pub.total_bytes;
+  dv.is_compressed = h->is_compressed ? comp : nullptr;   // global_scores (F) is a device pool like K/V
   int rc = zpc_compress(d, p, &dv, stream);
   if (rc != ZPC_OK) return rc;
   if (R) {

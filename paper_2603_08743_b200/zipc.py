@@ -33,6 +33,7 @@ ZPC_F_VALIDATE = 2
 ZPC_F_COUNT_MOVES = 4
 ZPC_F_SCORE_CUDACORE = 8
 ZPC_F_REDUNDANCY = 16
+ZPC_F_GLOBAL_SCORE = 32
 
 ZPC_MAX_SEQ_LEN = 49152
 
@@ -54,7 +55,7 @@ class zpc_cache_desc(ctypes.Structure):
 class zpc_params(ctypes.Structure):
     _fields_ = [("n_max", I32), ("pool_kernel", I32), ("max_seq_len", I32), ("flags", ctypes.c_uint32),
                 ("redundancy_lambda", ctypes.c_float), ("redundancy_tau", ctypes.c_float),
-                ("redundancy_p", ctypes.c_float)]
+                ("redundancy_p", ctypes.c_float), ("global_alpha", ctypes.c_float)]
 
 
 class zpc_batch(ctypes.Structure):
@@ -63,7 +64,8 @@ class zpc_batch(ctypes.Structure):
                 ("budgets", P), ("new_lens", P), ("new_num_blocks", P), ("ref_counts", P),
                 ("free_stack", P), ("free_top", P), ("free_capacity", I32),
                 ("freed_blocks", P), ("num_freed", P), ("freed_capacity", I32),
-                ("workspace", P), ("workspace_bytes", ctypes.c_size_t), ("status", P)]
+                ("workspace", P), ("workspace_bytes", ctypes.c_size_t), ("status", P),
+                ("global_scores", P), ("is_compressed", P)]
 
 
 class zpc_workspace_layout(ctypes.Structure):
@@ -118,10 +120,11 @@ def make_desc(L, h_kv, h_q, d, b, N_total, M, w, dtype) -> zpc_cache_desc:
 
 
 def make_params(n_max, pool_kernel=1, max_seq_len=ZPC_MAX_SEQ_LEN, flags=0, redundancy_lambda=0.2,
-                redundancy_tau=0.4, redundancy_p=0.8) -> zpc_params:
+                redundancy_tau=0.4, redundancy_p=0.8, global_alpha=0.8) -> zpc_params:
     """redundancy_*: used with ZPC_F_REDUNDANCY (PAPER.md:718 recommends lambda 0.2, tau 0.4; the paper
-    gives no value for p, 0.8 is a placeholder)."""
-    return zpc_params(n_max, pool_kernel, max_seq_len, flags, redundancy_lambda, redundancy_tau, redundancy_p)
+    gives no value for p, 0.8 is a placeholder); global_alpha with ZPC_F_GLOBAL_SCORE (0.8, :718)."""
+    return zpc_params(n_max, pool_kernel, max_seq_len, flags, redundancy_lambda, redundancy_tau, redundancy_p,
+                      global_alpha)
 
 
 def zpc_workspace_bytes(desc, params, R) -> int:
@@ -149,7 +152,7 @@ def _ptr(t):
 
 def make_batch(*, k_cache, v_cache, q_cache, q_slots, seq_lens, block_tables, budgets, new_lens,
                new_num_blocks, ref_counts, free_stack, free_top, freed_blocks, num_freed, workspace,
-               status) -> zpc_batch:
+               status, global_scores=None, is_compressed=None) -> zpc_batch:
     """All arguments are torch tensors (device for zpc_compress; see zipc.h for the host variant)."""
     return zpc_batch(
         _ptr(k_cache), _ptr(v_cache), _ptr(q_cache), int(seq_lens.numel()),
@@ -157,7 +160,8 @@ def make_batch(*, k_cache, v_cache, q_cache, q_slots, seq_lens, block_tables, bu
         _ptr(budgets), _ptr(new_lens), _ptr(new_num_blocks), _ptr(ref_counts),
         _ptr(free_stack), _ptr(free_top), int(free_stack.numel()),
         _ptr(freed_blocks), _ptr(num_freed), int(freed_blocks.numel()),
-        _ptr(workspace), int(workspace.numel() * workspace.element_size()), _ptr(status))
+        _ptr(workspace), int(workspace.numel() * workspace.element_size()), _ptr(status),
+        _ptr(global_scores), _ptr(is_compressed))
 
 
 def _stream(stream):

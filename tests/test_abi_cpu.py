@@ -85,3 +85,13 @@ def test_compress_rejects_bad_args_before_enqueueing():
                        free_stack=addr, free_top=addr, freed_blocks=addr, num_freed=addr)
     assert zipc.zpc_compress(d, p, b, stream=0, check=False) == zipc.ZPC_ERR_WORKSPACE
     assert zipc.status_string(zipc.ZPC_ERR_NO_FREE_BLOCKS).startswith("free stack")
+
+
+def test_global_score_params():
+    """ZPC_F_GLOBAL_SCORE validates alpha in [0, 1]; without the flag alpha is ignored."""
+    for bad in (-0.1, 1.5, float("inf")):
+        assert zipc.zpc_workspace_bytes(_desc(), zipc.make_params(129, 7, 8192, zipc.ZPC_F_GLOBAL_SCORE,
+                                                                  global_alpha=bad), 4) == 0
+        assert zipc.zpc_workspace_bytes(_desc(), zipc.make_params(129, 7, 8192, 0, global_alpha=bad), 4) > 0
+    assert zipc.zpc_workspace_bytes(_desc(), zipc.make_params(129, 7, 8192, zipc.ZPC_F_GLOBAL_SCORE,
+                                                              global_alpha=0.8), 4) > 0

@@ -78,6 +78,8 @@ class DeviceWorkload:
     status: torch.Tensor
     workspace: torch.Tensor | None = None
     max_seq_len: int = 0
+    f_cache: torch.Tensor | None = None          # NEXT-2 global-score pool
+    is_compressed: torch.Tensor | None = None    # NEXT-2 [R]
 
 
 def alloc_outputs(R, L, h_kv, N_total, freed_capacity, device="cuda"):
@@ -105,7 +107,10 @@ def from_host(hw, device="cuda", max_seq_len=None) -> DeviceWorkload:
         ref_counts=None if lay.ref_counts is None else to_dev(lay.ref_counts, device),
         free_stack=to_dev(lay.free_stack, device),
         free_top=torch.tensor([lay.free_top], dtype=torch.int32, device=device),
-        max_seq_len=int(max_seq_len or int(lay.seq_lens.max())), **outs)
+        max_seq_len=int(max_seq_len or int(lay.seq_lens.max())),
+        f_cache=None if getattr(hw, "f_cache", None) is None else to_dev(hw.f_cache, device),
+        is_compressed=None if getattr(hw, "is_compressed", None) is None else to_dev(hw.is_compressed, device),
+        **outs)
 
 
 def generate(cfg: Config, seed: int, rids, device="cuda", table_stride=None) -> DeviceWorkload:

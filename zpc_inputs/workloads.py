@@ -261,6 +261,8 @@ class HostWorkload:
     k_cache: np.ndarray
     v_cache: np.ndarray
     q_cache: np.ndarray
+    f_cache: np.ndarray | None = None        # NEXT-2 global-score pool (global_history)
+    is_compressed: np.ndarray | None = None  # NEXT-2 [R]
 
 
 def make_host_workload(cfg: Config, seed: int, rids=None, table_stride=None) -> HostWorkload:
@@ -282,3 +284,22 @@ def make_host_workload(cfg: Config, seed: int, rids=None, table_stride=None) -> 
             Q[l, lay.q_slots[i]] = q_rows(cfg, seed, int(rid), l)
     return HostWorkload(cfg=cfg, seed=seed, layout=lay, budgets=budgets_for(cfg, seed, lay.rids),
                         k_cache=K, v_cache=V, q_cache=Q)
+
+
+# ------------------------------------------------------------------ NEXT-2 inputs (random numbers only)
+KIND_GLOBAL = 9
+
+
+def global_history(cfg: Config, seed, N_total: int, rids, scale=None):
+    """Previous global scores F [L, N_total, b, h_kv] fp32 (Philox uniform in [0, scale); scale ~ the
+    mean attention score 2/T) and is_compressed [R] int32 (every even global request id has been
+    compressed before). Seeded random inputs, no method arithmetic."""
+    rids = np.asarray(rids)
+    if scale is None:
+        scale = 2.0 / float(np.mean([cfg.seq_lens[int(r)] for r in rids]))
+    n = cfg.L * N_total * cfg.b * cfg.h_kv
+    x0, _, _, _ = philox4x32(np.arange(n, dtype=np.uint32), np.uint32(0), np.uint32(KIND_GLOBAL << 24),
+                             np.uint32(0), seed & 0xFFFFFFFF, (seed >> 32) & 0xFFFFFFFF)
+    f = ((x0 >> 8).astype(np.float64) * (1.0 / (1 << 24)) * scale).astype(np.float32)
+    comp = (rids % 2 == 0).astype(np.int32)
+    return f.reshape(cfg.L, N_total, cfg.b, cfg.h_kv), comp
