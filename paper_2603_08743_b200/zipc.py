@@ -13,6 +13,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 # ZPC_LIB: an alternative build of the same library (A/B timing of two builds on one GPU box)
 LIB_PATH = os.environ.get("ZPC_LIB") or os.path.join(HERE, "lib", "libzipc.so")
 
+ABI_VERSION = 2  # include/zipc.h ZPC_ABI_VERSION
+
 ZPC_OK = 0
 ZPC_ERR_INVALID_ARG = -1
 ZPC_ERR_WORKSPACE = -2
