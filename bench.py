@@ -211,12 +211,14 @@ def redundancy_roofline(cfg, seq_lens, world, red_ms, peaks):
 
 
 # ---------------------------------------------------------------- GPU arm
-def algorithmic_bytes(cfg, seq_lens, budgets, moves):
-    """SURVEY §8(d) per-unit algorithmic bytes summed over the batch."""
+def algorithmic_bytes(cfg, seq_lens, budgets, moves, lse_input=False):
+    """SURVEY §8(d) per-unit algorithmic bytes summed over the batch (+ the 4*G*w normaliser bytes a
+    unit reads with ZPC_F_LSE_INPUT)."""
     e = 2 if cfg.dtype == "bf16" else 4
     T = np.asarray(seq_lens, np.int64)
     units_per_req = cfg.L * cfg.h_kv
-    score = int((T * cfg.d * e + cfg.G * cfg.w * cfg.d * e + 4 * T).sum() * units_per_req)
+    score = int((T * cfg.d * e + cfg.G * cfg.w * cfg.d * e + 4 * T + (4 * cfg.G * cfg.w if lse_input else 0)).sum()
+                * units_per_req)
     ell = np.minimum(np.asarray(budgets, np.int64), T[:, None, None])
     select = int((4 * T).sum() * units_per_req + 4 * ell.sum())
     compact = int(4 * moves * cfg.d * e)
@@ -238,6 +240,10 @@ def main():
     ap.add_argument("--redundancy", action="store_true",
                     help="NEXT-1: lightning redundancy + temperature softmax in the selection score "
                          "(lambda 0.2, tau 0.4 as PAPER.md:718 recommends; p 0.8, the paper gives none)")
+    ap.add_argument("--lse-input", action="store_true",
+                    help="NEXT-4: single-pass scoring with the window normalisers supplied (ZPC_F_LSE_INPUT); "
+                         "the normalisers a decode engine would hold are produced untimed by one two-pass "
+                         "zpc_score call before the timed steps")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -250,7 +256,8 @@ def main():
     workload = (f"{cfg.name}: {per_gpu} req/GPU x {cfg.seq_lens[0]} tok, L={cfg.L} h_kv={cfg.h_kv} h_q={cfg.h_q} "
                 f"d={cfg.d} b={cfg.b} w={cfg.w} N_max={cfg.n_max} budget={cfg.budget} pool={cfg.pool_kernel}"
                 + (f" prefix={cfg.prefix_tokens}" if cfg.prefix_tokens else "")
-                + (" + NEXT-1 lightning redundancy (lambda=0.2 tau=0.4 p=0.8)" if args.redundancy else ""))
+                + (" + NEXT-1 lightning redundancy (lambda=0.2 tau=0.4 p=0.8)" if args.redundancy else "")
+                + (" + NEXT-4 window LSE input (single-pass score)" if args.lse_input else ""))
 
     if args.impl == "reference":
         if rank != 0:
@@ -284,13 +291,16 @@ def main():
     dev = torch.device("cuda", torch.cuda.current_device())
 
     from paper_2603_08743_b200 import zipc
-    from paper_2603_08743_b200.batch import batch_of, desc_params
+    from paper_2603_08743_b200.batch import batch_of, desc_params, window_lse_from_two_pass
     from zpc_inputs.device import generate
 
     rids = shard_rids(rank, world, per_gpu, cfg.R)
     w = generate(cfg, args.seed, rids, device=dev)
     flags = zipc.ZPC_F_COUNT_MOVES | (zipc.ZPC_F_SCORE_CUDACORE if args.cudacore else 0)
-    desc, params = desc_params(w, flags=flags, redundancy=RED_PARAMS if args.redundancy else None)
+    if args.lse_input:
+        w.window_lse = window_lse_from_two_pass(w, flags)
+    desc, params = desc_params(w, flags=flags, redundancy=RED_PARAMS if args.redundancy else None,
+                               lse_input=args.lse_input)
     batch = batch_of(w, desc, params)
     stream = torch.cuda.current_stream()
     lay = w.layout
@@ -362,20 +372,21 @@ def main():
     T_sum = int(lay.seq_lens.sum())
 
     peaks = load_peaks()
-    ab = algorithmic_bytes(cfg, lay.seq_lens, w.budgets_host, moves)
+    ab = algorithmic_bytes(cfg, lay.seq_lens, w.budgets_host, moves, args.lse_input)
     score_ms = stage_ms[stage_names.index("score")] / args.steps
     compact_ms = stage_ms[stage_names.index("compact")] / args.steps
     step_bytes = ab["score"] + ab["select"] + ab["compact"]
-    traffic = measured_traffic(cfg, per_gpu)
+    traffic = {} if args.lse_input else measured_traffic(cfg, per_gpu)
     roofline = {"kernel": "score (a1+a2)", "bound": "hbm", "achieved": ab["score"] / (score_ms / 1e3) / 1e9,
                 "peak": peaks["hbm"], "unit": "GB/s", "peak_src": peaks["src"],
                 "traffic": traffic.get("score"), "traffic_unit": "bytes/launch (dram read+write, ncu --set full)",
                 "algorithmic_bytes_per_launch": ab["score"]}
     roofline["frac"] = roofline["achieved"] / roofline["peak"]
-    tensor_tf = ab["flops_score"] * 2 / (score_ms / 1e3) / 1e12   # two passes of 2*G*w*d per token
+    passes = 1 if args.lse_input else 2
+    tensor_tf = ab["flops_score"] * passes / (score_ms / 1e3) / 1e12   # passes x 2*G*w*d per token
     extra = {
         "stage_ms": {n: round(float(x) / args.steps, 4) for n, x in zip(stage_names, stage_ms)},
-        "score_tensor_tflops_two_pass": tensor_tf,
+        "score_tensor_tflops": tensor_tf, "score_passes": passes,
         "compact_roofline": {"achieved": ab["compact"] / (compact_ms / 1e3) / 1e9 if compact_ms else None,
                              "peak": peaks["hbm"], "unit": "GB/s", "moved_rows": moves,
                              "frac": (ab["compact"] / (compact_ms / 1e3) / 1e9) / peaks["hbm"] if compact_ms else None,
@@ -405,7 +416,7 @@ def main():
                              new_lens=host["new_lens"], new_num_blocks=host["new_num_blocks"], ref_counts=href_live,
                              free_stack=host_live["free_stack"], free_top=host_live["free_top"],
                              freed_blocks=host["freed"], num_freed=host["num_freed"], workspace=ws_h,
-                             status=host["status"])
+                             status=host["status"], window_lse=w.window_lse)
         R = len(rids)
         h2d = 4 * (R * 2 + R * lay.table_stride + host["budgets"].numel() + lay.N_total + 1) + \
             (4 * lay.N_total if href is not None else 0)

@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define ZPC_ABI_VERSION 2
+#define ZPC_ABI_VERSION 3
 
 /* ---- return / status codes ---- */
 #define ZPC_OK                  0
@@ -54,7 +54,7 @@ extern "C" {
                                        ZPC_F_REDUNDANCY with lambda < 0, tau <= 0, p outside [0,1],
                                        a non-finite value or block_size > 32, ZPC_F_GLOBAL_SCORE
                                        with alpha outside [0,1] or a NULL global_scores /
-                                       is_compressed */
+                                       is_compressed, ZPC_F_LSE_INPUT with a NULL window_lse */
 #define ZPC_ERR_WORKSPACE      -2   /* workspace_bytes < zpc_workspace_bytes(...) */
 #define ZPC_ERR_CUDA           -3   /* a launch failed (cudaGetLastError) */
 #define ZPC_ERR_NOT_TRIGGERED -10   /* device: N = ceil(T/b) < N_max */
@@ -90,6 +90,14 @@ extern "C" {
                                  pooling etc. then use the updated S, and compaction moves each kept
                                  row's F with its K/V. Needs batch.global_scores and
                                  batch.is_compressed; params.global_alpha. */
+#define ZPC_F_LSE_INPUT 64u   /* NEXT-4: single-pass scoring. batch.window_lse supplies, per layer, query
+                                 slot, window row u and query head, the softmax normaliser
+                                 LSE = log sum_{t <= T-w+u} exp(q.k_t / sqrt(d)) (natural log) that the
+                                 decode attention of position T-w+u already computed (it attends over
+                                 exactly the keys 0..T-w+u). a2 then needs one pass over K instead of
+                                 two: S[t] = (1/w) sum_u max_g exp(q.k_t/sqrt(d) - LSE[u][g])
+                                 (PAPER.md:409-411 with the normaliser given). Results equal the
+                                 two-pass ones when the input is the exact normaliser. */
 
 /* Pool geometry: K, V [L][N_total][b][h_kv][d], Q [L][M][w][h_q][d].
  * Q row u of slot j holds the query of position T-w+u of the request bound to slot j (R3). */
@@ -167,6 +175,11 @@ typedef struct {
    *   is_compressed  dev int32 [R], 0 or 1: the request was compressed before (Alg. 2 line 3) */
   float* global_scores;
   const int32_t* is_compressed;
+  /* ZPC_F_LSE_INPUT only (else ignored, may be NULL):
+   *   window_lse  dev fp32 [L][M][w][h_q], natural log, laid out like the Q cache without d: entry
+   *               (l, j, u, i) is the log-sum-exp of query head i of window row u of slot j over keys
+   *               0..T-w+u, logits scaled by 1/sqrt(d). Must be finite. Read only. */
+  const float* window_lse;
 } zpc_batch;
 
 /* Where intermediate results live inside the workspace (byte offsets; all 256-B aligned). */

@@ -260,13 +260,57 @@ def attention_scores(A: np.ndarray, T: int) -> np.ndarray:
     return P.max(axis=0).mean(axis=0)      # max over g, then mean over u
 
 
+# --------------------------------------------------------------------------
+# NEXT-4: single-pass scoring with the window normalisers given (derived from
+# PAPER.md:409-411). The softmax of window row u is exp(A[g,u,t] - LSE[g,u]) with
+# LSE[g,u] = log sum_{t <= T-w+u} exp(A[g,u,t]); decode attention of position T-w+u attends over exactly
+# the keys 0..T-w+u with the same 1/sqrt(d) logits, so a serving engine already holds LSE.
+# --------------------------------------------------------------------------
+def window_lse(A: np.ndarray, T: int) -> np.ndarray:
+    """LSE[g, u] = log sum_t exp(A[g, u, t]) over the unmasked entries (natural log), A as in
+    attention_scores. The normaliser of PAPER.md:409's softmax, written out."""
+    A = A[:, :, :T]
+    m = A.max(axis=2)
+    return m + np.log(np.exp(A - m[:, :, None]).sum(axis=2))
+
+
+def attention_scores_given_lse(A: np.ndarray, lse: np.ndarray, T: int) -> np.ndarray:
+    """s[t] = (1/w) sum_u max_g exp(A[g,u,t] - lse[g,u]) (PAPER.md:409-411 with the softmax normaliser
+    supplied instead of recomputed). Equals attention_scores(A, T) when lse = window_lse(A, T)."""
+    P = np.exp(A[:, :, :T] - lse[:, :, None])    # masked entries: exp(-inf) = 0
+    return P.max(axis=0).mean(axis=0)
+
+
+def unit_window_lse(geo: Geometry, window_lse_in: np.ndarray, slot: int, l: int, h: int) -> np.ndarray:
+    """[G, w] slice of a window_lse array laid out [L][M][w][h_q] (the ABI's layout), group of KV head h
+    (R5)."""
+    return np.asarray(window_lse_in[l, slot][:, list(_group(geo, h))], np.float64).T
+
+
 def unit_scores(geo: Geometry, q_cache_f64, k_pool_f64, table, T: int, slot: int, l: int, h: int,
-                blockwise: bool = False) -> np.ndarray:
-    """S for one unit (request, layer, KV head) from widened caches."""
+                blockwise: bool = False, window_lse_in=None) -> np.ndarray:
+    """S for one unit (request, layer, KV head) from widened caches; with window_lse_in
+    ([L][M][w][h_q]) the normalisers are taken from it (NEXT-4)."""
     q = q_cache_f64[l, slot]           # [w, h_q, d]
     kl = k_pool_f64[l]                 # [N_total, b, h_kv, d]
     A = (logits_blockwise if blockwise else logits_dense)(geo, q, kl, table, T, h)
+    if window_lse_in is not None:
+        return attention_scores_given_lse(A, unit_window_lse(geo, window_lse_in, slot, l, h), T)
     return attention_scores(A, T)
+
+
+def all_window_lse(geo: Geometry, q_cache, k_cache, q_slots, seq_lens, tables) -> np.ndarray:
+    """The [L][M][w][h_q] normaliser array a decode engine would hold for these requests (slots not
+    bound to a request stay 0): window_lse of every unit, by definition."""
+    out = np.zeros((geo.L, geo.M, geo.w, geo.h_q))
+    qf, kf = widen(q_cache, geo.dtype), widen(k_cache, geo.dtype)
+    for r in range(len(seq_lens)):
+        T, slot = int(seq_lens[r]), int(q_slots[r])
+        for l in range(geo.L):
+            for h in range(geo.h_kv):
+                A = logits_dense(geo, qf[l, slot], kf[l], tables[r], T, h)
+                out[l, slot][:, list(_group(geo, h))] = window_lse(A, T).T
+    return out
 
 
 # --------------------------------------------------------------------------
@@ -527,12 +571,14 @@ class CompressOut:
 
 def compress(geo: Geometry, prm: Params, k_cache, v_cache, q_cache, q_slots, seq_lens, tables, budgets,
              ref_counts=None, free_stack=None, free_top=0, kept_override=None, blockwise=False,
-             free_capacity=None, freed_capacity=None, units=None, f_cache=None, is_compressed=None) -> CompressOut:
+             free_capacity=None, freed_capacity=None, units=None, f_cache=None, is_compressed=None,
+             window_lse_in=None) -> CompressOut:
     """Steps 1-9 of SURVEY.md §8(c) for every request r (input order), layer l, KV head h.
 
     kept_override: optional dict (r, l, h) -> kept list, used to drive compaction with
     a kept set chosen elsewhere (the 'bytes' parity rule). units: optional subset of
     (r, l, h) to score (for sampled checks); compaction then needs kept_override.
+    window_lse_in: optional [L][M][w][h_q] natural-log normalisers (NEXT-4, ZPC_F_LSE_INPUT).
     """
     pl = plan(geo, prm, seq_lens, tables, budgets, ref_counts, free_stack, free_top, q_slots,
               free_capacity, freed_capacity)
@@ -557,13 +603,13 @@ def compress(geo: Geometry, prm: Params, k_cache, v_cache, q_cache, q_slots, seq
                 if kept_override is not None and key in kept_override:
                     kept = np.asarray(kept_override[key], np.int32)
                     if use_global:   # F is still updated by Alg. 2 before it is relocated
-                        s = unit_scores(geo, qf, kf, tables[r], T, int(q_slots[r]), l, h, blockwise)
+                        s = unit_scores(geo, qf, kf, tables[r], T, int(q_slots[r]), l, h, blockwise, window_lse_in)
                         gscores[key] = global_score_update(s, f_out[l], tables[r], T, h, geo.b, prm.n_max,
                                                            bool(is_compressed[r]), prm.alpha)
                 else:
                     if units is not None and key not in units:
                         continue
-                    s = unit_scores(geo, qf, kf, tables[r], T, int(q_slots[r]), l, h, blockwise)
+                    s = unit_scores(geo, qf, kf, tables[r], T, int(q_slots[r]), l, h, blockwise, window_lse_in)
                     scores[key] = s
                     if use_global:
                         s = global_score_update(s, f_out[l], tables[r], T, h, geo.b, prm.n_max,

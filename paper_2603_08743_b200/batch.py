@@ -11,9 +11,11 @@ import torch
 from . import zipc
 
 
-def desc_params(w, flags=0, pool_kernel=None, max_seq_len=None, redundancy=None, global_alpha=None):
+def desc_params(w, flags=0, pool_kernel=None, max_seq_len=None, redundancy=None, global_alpha=None,
+                lse_input=False):
     """redundancy: None, or (lambda, tau, p) -> sets ZPC_F_REDUNDANCY with those parameters.
-    global_alpha: None, or alpha -> sets ZPC_F_GLOBAL_SCORE (w.f_cache / w.is_compressed must exist)."""
+    global_alpha: None, or alpha -> sets ZPC_F_GLOBAL_SCORE (w.f_cache / w.is_compressed must exist).
+    lse_input: sets ZPC_F_LSE_INPUT (w.window_lse must exist: fp32 [L][M][w][h_q])."""
     cfg, lay = w.cfg, w.layout
     desc = zipc.make_desc(cfg.L, cfg.h_kv, cfg.h_q, cfg.d, cfg.b, lay.N_total, lay.M, cfg.w, cfg.dtype)
     if w.ref_counts is not None:
@@ -22,6 +24,8 @@ def desc_params(w, flags=0, pool_kernel=None, max_seq_len=None, redundancy=None,
     if global_alpha is not None:
         flags |= zipc.ZPC_F_GLOBAL_SCORE
         extra["global_alpha"] = global_alpha
+    if lse_input:
+        flags |= zipc.ZPC_F_LSE_INPUT
     if redundancy is not None:
         flags |= zipc.ZPC_F_REDUNDANCY
         extra.update(redundancy_lambda=redundancy[0], redundancy_tau=redundancy[1], redundancy_p=redundancy[2])
@@ -46,7 +50,8 @@ def batch_of(w, desc, params):
                            new_num_blocks=w.new_num_blocks, ref_counts=w.ref_counts, free_stack=w.free_stack,
                            free_top=w.free_top, freed_blocks=w.freed, num_freed=w.num_freed,
                            workspace=w.workspace, status=w.status,
-                           global_scores=getattr(w, "f_cache", None), is_compressed=getattr(w, "is_compressed", None))
+                           global_scores=getattr(w, "f_cache", None), is_compressed=getattr(w, "is_compressed", None),
+                           window_lse=getattr(w, "window_lse", None))
 
 
 def workspace_view(w, desc, params, name, dtype, shape):
@@ -58,3 +63,23 @@ def workspace_view(w, desc, params, name, dtype, shape):
         n *= s
     esz = torch.tensor([], dtype=dtype).element_size()
     return w.workspace[off:off + n * esz].view(dtype).view(*shape)
+
+
+def window_lse_from_two_pass(w, flags=0):
+    """NEXT-4 input for benchmarks and full-size tests: the fp32 [L][M][w][h_q] natural-log window
+    normalisers a decode engine would hold, produced by one two-pass zpc_plan + zpc_score call (its
+    LSE workspace region is [R][L][h_kv][w][G], log2 domain) and scattered to the query slots.
+    Leaves w.status reset; w.workspace is reused."""
+    cfg, lay = w.cfg, w.layout
+    desc, params = desc_params(w, flags=flags)
+    b = batch_of(w, desc, params)
+    zipc.zpc_plan(desc, params, b)
+    zipc.zpc_score(desc, params, b)
+    R, G = int(w.seq_lens.numel()), cfg.h_q // cfg.h_kv
+    lse2 = workspace_view(w, desc, params, "lse", torch.float32, (R, cfg.L, cfg.h_kv, cfg.w, G))
+    nat = (lse2 / 1.4426950408889634).permute(1, 0, 3, 2, 4).reshape(cfg.L, R, cfg.w, cfg.h_q)
+    out = torch.zeros((cfg.L, lay.M, cfg.w, cfg.h_q), dtype=torch.float32, device=w.k.device)
+    out[:, w.q_slots.long()] = nat
+    torch.cuda.synchronize()
+    w.status.fill_(12345)
+    return out

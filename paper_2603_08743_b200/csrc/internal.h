@@ -52,6 +52,7 @@ struct Call {
   int32_t* status;
   float* f_cache;                     // ZPC_F_GLOBAL_SCORE: F [L][N_total][b][h_kv]
   const int32_t* is_compressed;       // ZPC_F_GLOBAL_SCORE: [R]
+  const float* lse_in;                // ZPC_F_LSE_INPUT: [L][M][w][h_q] natural-log normalisers, else NULL
   Ws ws;
 };
 

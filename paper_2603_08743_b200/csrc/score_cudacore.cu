@@ -2,7 +2,7 @@
 // break the 1e-3 tolerance) and the reference fallback for bf16 when the
 // tcgen05 kernel is disabled by ZPC_F_SCORE_CUDACORE.
 //
-// Two passes:
+// Two passes (with ZPC_F_LSE_INPUT pass 1 is replaced by k_lse_input):
 //   pass 1 (k_lse_cc, one CTA per unit, one thread per window column c = u*G + g):
 //          LSE2[c] = log2 sum_{t <= T-w+u} 2^{x2[c,t]},  x2 = (q.k) * log2(e)/sqrt(d)
 //   pass 2 (k_final_cc, one thread per token):
@@ -75,6 +75,23 @@ __global__ void __launch_bounds__(kLseThreads) k_lse_cc(Call c) {
   if (active) c.ws.lse[(size_t)unit * GW + col] = m + lg2f(s);
 }
 
+// NEXT-4 (ZPC_F_LSE_INPUT): the normalisers come from the caller (the decode attention of each
+// window position), so pass 1 is a relayout: LSE2[unit][u*G + g] = log2(e) * lse_in[l][slot][u][h*G + g].
+__global__ void __launch_bounds__(kLseThreads) k_lse_input(Call c) {
+  if (*c.status != ZPC_OK) return;
+  const int unit = blockIdx.x;
+  const int h = unit % c.h_kv;
+  const int l = (unit / c.h_kv) % c.L;
+  const int r = unit / (c.h_kv * c.L);
+  const int slot = c.q_slots[r];
+  const int GW = c.G * c.w;
+  for (int col = threadIdx.x; col < GW; col += kLseThreads) {
+    const int u = col / c.G, g = col % c.G;
+    const size_t at = (((size_t)l * c.M + slot) * c.w + u) * c.h_q + (size_t)h * c.G + g;
+    c.ws.lse[(size_t)unit * GW + col] = c.lse_in[at] * 1.4426950408889634f;
+  }
+}
+
 template <typename E, int D>
 __global__ void __launch_bounds__(kFinThreads) k_final_cc(Call c) {
   if (*c.status != ZPC_OK) return;
@@ -131,7 +148,8 @@ template <typename E, int D>
 cudaError_t launch_typed(const Call& c, cudaStream_t s) {
   const int units = c.R * c.L * c.h_kv;
   if (units == 0) return cudaSuccess;
-  k_lse_cc<E, D><<<units, kLseThreads, 0, s>>>(c);
+  if (c.lse_in) k_lse_input<<<units, kLseThreads, 0, s>>>(c);
+  else k_lse_cc<E, D><<<units, kLseThreads, 0, s>>>(c);
   const size_t smem = sizeof(float) * ((size_t)c.G * c.w * D + (size_t)c.G * c.w);
   cudaFuncSetAttribute(k_final_cc<E, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   dim3 grid((c.max_seq_len + kFinThreads - 1) / kFinThreads, units);

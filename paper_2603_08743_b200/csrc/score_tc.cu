@@ -443,7 +443,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
   const float scale = kLog2e * rsqrtf((float)D);
 
   // per-unit geometry, identical in every role
-  struct UnitInfo { int r, l, h, T, slot, tb, nt; };
+  // NEXT-4 (ZPC_F_LSE_INPUT): the normalisers are an input, so a unit runs only pass 2 (p1 = 0)
+  const bool one_pass = c.lse_in != nullptr;
+  struct UnitInfo { int r, l, h, T, slot, tb, nt, p1; };
   auto unit_info = [&](int unit) {
     UnitInfo u;
     u.h = unit % c.h_kv;
@@ -454,11 +456,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
     const int ntot = (u.T + kTile - 1) / kTile;
     u.tb = (int)((long long)ntot * rank / C);
     u.nt = (int)((long long)ntot * (rank + 1) / C) - u.tb;
+    u.p1 = one_pass ? 0 : u.nt;          // pass-1 steps; the unit has p1 + nt steps in all
     return u;
   };
   // step i of a unit -> tile index: pass 1 ascending, pass 2 DESCENDING (the most recently
   // streamed tiles are the ones most likely still in L2)
-  auto tile_of = [](const UnitInfo& u, int i) { return i < u.nt ? u.tb + i : u.tb + (2 * u.nt - 1 - i); };
+  auto tile_of = [](const UnitInfo& u, int i) { return i < u.p1 ? u.tb + i : u.tb + (u.p1 + u.nt - 1 - i); };
 
   // register rebalance per warpgroup (setmaxnreg must dominate each role's code so ptxas
   // allocates the epilogue with kEpiRegs): the producers need few registers, the epilogue's latency
@@ -507,7 +510,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
     const uint32_t dst_thr = (uint32_t)rsub * 128u + (uint32_t)(((cr & 7) ^ (rsub & 7)) << 4) + chunk_off;
     const uint32_t hD = (uint32_t)c.h_kv * D;              // elements between consecutive slots
     auto issue_next_load = [&]() {
-      while (ld_unit < units && ld_i >= 2 * ld_u.nt) {
+      while (ld_unit < units && ld_i >= ld_u.p1 + ld_u.nt) {
         ld_unit += nclusters;
         ld_i = 0;
         if (ld_unit < units) ld_u = unit_info(ld_unit);
@@ -590,7 +593,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
     int f_unit = cluster_id, f_i = 0;
     UnitInfo f_u = f_unit < units ? unit_info(f_unit) : UnitInfo{};
     for (int g = 0;; ++g) {
-      while (f_unit < units && f_i >= 2 * f_u.nt) {
+      while (f_unit < units && f_i >= f_u.p1 + f_u.nt) {
         f_unit += nclusters;
         f_i = 0;
         if (f_unit < units) f_u = unit_info(f_unit);
@@ -621,7 +624,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
     for (int it = 0, unit = cluster_id; unit < units; ++it, unit += nclusters) {
       const UnitInfo u = unit_info(unit);
       mbar_wait(qfull0, it & 1);
-      for (int i = 0; i < 2 * u.nt; ++i, ++kstep, ++astep) {
+      for (int i = 0; i < u.p1 + u.nt; ++i, ++kstep, ++astep) {
         const int s = kstep % K::ST, a = astep & 1;
         const bool mrec = (c.debug & 1u) && blockIdx.x == 0 && astep < 1024 && lane == 0;
         unsigned long long* mdbg = reinterpret_cast<unsigned long long*>(c.ws.kept);
@@ -629,7 +632,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
         mbar_wait(acce0 + 8 * a, ((astep >> 1) & 1) ^ 1);
         if (mrec) mdbg[16384 + astep * 4 + 1] = gtimer();
         if (!(c.debug & 2048u)) mbar_wait(full0 + 8 * s, (kstep / K::ST) & 1);
-        if (i == u.nt) mbar_wait(augf, it & 1);   // this unit's -L2/s is in B_aug
+        if (i == u.p1) mbar_wait(augf, it & 1);   // this unit's -L2/s is in B_aug
         if (mrec) mdbg[16384 + astep * 4 + 2] = gtimer();
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // cp.async data -> tensor core
         tc_fence_after();
@@ -638,7 +641,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
         // descriptor start addresses are in 16-B units: a byte offset o adds o >> 4
         if (c.debug & 4u) {
           // debug: no MMA
-        } else if (i < u.nt) {
+        } else if (i < u.p1) {
 #pragma unroll
           for (int half = 0; half < K::M1H; ++half)
 #pragma unroll
@@ -684,6 +687,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // visible to the tensor core
     };
     int astep = 0;
+    // NEXT-4: caller's natural-log normaliser of this thread's column (u1, g) for a unit
+    auto lse_input = [&](int un) {
+      const int h = un % c.h_kv, l = (un / c.h_kv) % c.L, r = un / (c.h_kv * c.L);
+      return __ldg(c.lse_in + (((size_t)l * c.M + c.q_slots[r]) * W + u1) * c.h_q + (size_t)h * G + (col - u1 * G));
+    };
+    float lse_next = 0.f;
     // debug timing (bit 1): [0] P1 step work, [2] P1 gap before step, [3] P2 ld, [4] P2 math, [5] P2 gap,
     // [1] P1 steps, [6] P2 work (start..end), [7] P2 steps
     uint32_t tacc[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tlast = (uint32_t)gtimer();
@@ -691,8 +700,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
       const UnitInfo u = unit_info(unit);
       const int limit1 = u.T - W + u1;   // pass-1 causal limit of this column (R1, R2)
       float m = -INFINITY, ssum = 0.f, m1 = -INFINITY, s1 = 0.f;   // two pass-1 streams (see pair())
-      for (int i = 0; i <= 2 * u.nt; ++i) {
-        if (i == u.nt) {
+      for (int i = 0; i <= u.p1 + u.nt; ++i) {
+        if (i == u.p1) {
           // ---- end of pass 1: LSE per column, combined across the cluster through DSMEM
           {   // merge the two streams into (m, ssum)
             const float mm = fmaxf(m, m1);
@@ -701,7 +710,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
             m = mm;
           }
           const int pb = it & 1;
-          if (C == 1) {
+          if (one_pass) {
+            // NEXT-4: the normaliser of column (u, g) is the caller's natural-log LSE of query head
+            // h*G + g at window row u; log2 domain like pass 1's
+            // (the next unit's value is loaded here too, so its latency is off the next boundary)
+            if (col_ok) {
+              const float L2 = (it == 0 ? lse_input(unit) : lse_next) * kLog2e;
+              if (unit + nclusters < units) lse_next = lse_input(unit + nclusters);
+              write_aug(col, L2);
+              if (rank == 0) c.ws.lse[(size_t)unit * K::GW + col] = L2;
+            }
+          } else if (C == 1) {
             if (col_ok) {
               const float L2 = m + lg2f(ssum);
               write_aug(col, L2);
@@ -735,7 +754,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
           }
           named_bar(1, kEpiWarps * 32);
           if (ew == 0 && lane == 0) mbar_arrive(augf);   // pass-2 MMAs of this unit may start
-          if (i == 2 * u.nt) break;
+          if (i == u.p1 + u.nt) break;
           continue;
         }
         const int a = astep & 1;
@@ -748,16 +767,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
         mbar_wait(accf0 + 8 * a, (astep >> 1) & 1);
         if (rec) dbg[8192 + astep * 4 + 1] = gtimer();
         const uint32_t ts0 = (c.debug & 1u) ? (uint32_t)gtimer() : 0u;   // per-warp register timing (mod 2^32)
-        if (c.debug & 1u) { tacc[(i < u.nt ? 0 : 3) + 2] += ts0 - tlast; }
+        if (c.debug & 1u) { tacc[(i < u.p1 ? 0 : 3) + 2] += ts0 - tlast; }
         tc_fence_after();
         if ((c.debug & 1u) && blockIdx.x == 0 && ew == 0 && lane == 0 && astep < 512)
           reinterpret_cast<unsigned long long*>(c.ws.kept)[astep * 4 + 2] = gtimer();
-        const int t0 = tile_of(u, i < u.nt ? i : i - 1) * kTile;
+        const int t0 = tile_of(u, i < u.p1 ? i : i - 1) * kTile;
         if (c.debug & 2u) {
           // debug: no epilogue math
           __syncwarp();
           if (lane == 0) mbar_arrive(acce0 + 8 * a);
-        } else if (i < u.nt) {
+        } else if (i < u.p1) {
           // ---- pass 1: this thread owns window column `col`; 128 token logits in TMEM, consumed
           //      as 4 batches of 32 with the next batch's TMEM load in flight during the math. The
           //      batch loop stays rolled (ping-pong pairs) so its body fits the L0 instruction cache.
@@ -862,7 +881,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
         if (rec) dbg[8192 + astep * 4 + 2] = gtimer();
         if (c.debug & 1u) {
           const uint32_t te = (uint32_t)gtimer();
-          if (i < u.nt) { tacc[0] += te - ts0; tacc[1] += 1; } else { tacc[6] += te - ts0; tacc[7] += 1; }
+          if (i < u.p1) { tacc[0] += te - ts0; tacc[1] += 1; } else { tacc[6] += te - ts0; tacc[7] += 1; }
           tlast = te;
         }
         ++astep;
@@ -934,18 +953,23 @@ cudaError_t launch_tc(const Call& c, const CUtensorMap& tq, cudaStream_t s) {
 
 // Cluster size: CTAs per unit. Splitting a unit's tokens over C CTAs shrinks the K slice each
 // CTA re-reads in pass 2 (in flight across the GPU: ~148/C slices), keeping it L2-resident
-// (DESIGN.md §Score kernel, L2 reuse). ZPC_SCORE_CLUSTER (1/2) overrides, for tuning runs.
+// (DESIGN.md §Score kernel, L2 reuse). ZPC_SCORE_CLUSTER (1/2/4/8) overrides, for tuning runs.
 int cluster_size(const Call& c) {
   if (const char* e = getenv("ZPC_SCORE_CLUSTER")) {
     const int v = atoi(e);
-    if (v == 1 || v == 2) return v;
+    if (v == 1 || v == 2 || v == 4 || v == 8) return v;
   }
   return c.max_seq_len < 2 * kTile ? 1 : 2;
 }
 
 template <int G, int W, int D>
 cudaError_t launch_c(const Call& c, const CUtensorMap& tq, cudaStream_t s) {
-  return cluster_size(c) == 2 ? launch_tc<G, W, D, 2>(c, tq, s) : launch_tc<G, W, D, 1>(c, tq, s);
+  switch (cluster_size(c)) {
+    case 8: return launch_tc<G, W, D, 8>(c, tq, s);
+    case 4: return launch_tc<G, W, D, 4>(c, tq, s);
+    case 2: return launch_tc<G, W, D, 2>(c, tq, s);
+    default: return launch_tc<G, W, D, 1>(c, tq, s);
+  }
 }
 
 template <int D>

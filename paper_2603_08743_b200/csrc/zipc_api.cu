@@ -82,6 +82,7 @@ int make_call(const zpc_cache_desc* d, const zpc_params* p, const zpc_batch* b, 
   if (b->table_stride < 1 && b->num_requests > 0) return ZPC_ERR_INVALID_ARG;
   if ((p->flags & ZPC_F_PREFIX) && !b->ref_counts) return ZPC_ERR_INVALID_ARG;
   if ((p->flags & ZPC_F_GLOBAL_SCORE) && (!b->global_scores || !b->is_compressed)) return ZPC_ERR_INVALID_ARG;
+  if ((p->flags & ZPC_F_LSE_INPUT) && b->num_requests > 0 && !b->window_lse) return ZPC_ERR_INVALID_ARG;
   if ((reinterpret_cast<uintptr_t>(b->workspace) & (kAlign - 1)) != 0) return ZPC_ERR_INVALID_ARG;
   if (b->workspace_bytes < ls.pub.total_bytes) return ZPC_ERR_WORKSPACE;
   const int esz = d->dtype == ZPC_BF16 ? 2 : 4;
@@ -114,6 +115,7 @@ int make_call(const zpc_cache_desc* d, const zpc_params* p, const zpc_batch* b, 
   c->global_alpha = p->global_alpha;
   c->f_cache = b->global_scores;
   c->is_compressed = b->is_compressed;
+  c->lse_in = (p->flags & ZPC_F_LSE_INPUT) ? b->window_lse : nullptr;
   c->ws.req_err = reinterpret_cast<int32_t*>(w + ls.req_err);
   c->ws.n_blocks = reinterpret_cast<int32_t*>(w + ls.n_blocks);
   c->ws.fresh_off = reinterpret_cast<int32_t*>(w + ls.fresh_off);
@@ -245,7 +247,7 @@ int zpc_compress_host(const zpc_cache_desc* d, const zpc_params* p, const zpc_ba
   dv.new_lens = new_lens; dv.new_num_blocks = nnb; dv.ref_counts = h->ref_counts ? refs : nullptr;
   dv.free_stack = stack; dv.free_top = small; dv.freed_blocks = freed; dv.num_freed = small + 1;
   dv.status = small + 2; dv.workspace = h->workspace; dv.workspace_bytes = ls.pub.total_bytes;
-  dv.is_compressed = h->is_compressed ? comp : nullptr;   // global_scores (F) is a device pool like K/V
+  dv.is_compressed = h->is_compressed ? comp : nullptr;   // global_scores (F), window_lse: device, like K/V/Q
   int rc = zpc_compress(d, p, &dv, stream);
   if (rc != ZPC_OK) return rc;
   if (R) {

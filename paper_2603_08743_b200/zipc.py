@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 # ZPC_LIB: an alternative build of the same library (A/B timing of two builds on one GPU box)
 LIB_PATH = os.environ.get("ZPC_LIB") or os.path.join(HERE, "lib", "libzipc.so")
 
-ABI_VERSION = 2  # include/zipc.h ZPC_ABI_VERSION
+ABI_VERSION = 3  # include/zipc.h ZPC_ABI_VERSION
 
 ZPC_OK = 0
 ZPC_ERR_INVALID_ARG = -1
@@ -36,6 +36,7 @@ ZPC_F_COUNT_MOVES = 4
 ZPC_F_SCORE_CUDACORE = 8
 ZPC_F_REDUNDANCY = 16
 ZPC_F_GLOBAL_SCORE = 32
+ZPC_F_LSE_INPUT = 64
 
 ZPC_MAX_SEQ_LEN = 49152
 
@@ -67,7 +68,7 @@ class zpc_batch(ctypes.Structure):
                 ("free_stack", P), ("free_top", P), ("free_capacity", I32),
                 ("freed_blocks", P), ("num_freed", P), ("freed_capacity", I32),
                 ("workspace", P), ("workspace_bytes", ctypes.c_size_t), ("status", P),
-                ("global_scores", P), ("is_compressed", P)]
+                ("global_scores", P), ("is_compressed", P), ("window_lse", P)]
 
 
 class zpc_workspace_layout(ctypes.Structure):
@@ -154,7 +155,7 @@ def _ptr(t):
 
 def make_batch(*, k_cache, v_cache, q_cache, q_slots, seq_lens, block_tables, budgets, new_lens,
                new_num_blocks, ref_counts, free_stack, free_top, freed_blocks, num_freed, workspace,
-               status, global_scores=None, is_compressed=None) -> zpc_batch:
+               status, global_scores=None, is_compressed=None, window_lse=None) -> zpc_batch:
     """All arguments are torch tensors (device for zpc_compress; see zipc.h for the host variant)."""
     return zpc_batch(
         _ptr(k_cache), _ptr(v_cache), _ptr(q_cache), int(seq_lens.numel()),
@@ -163,7 +164,7 @@ def make_batch(*, k_cache, v_cache, q_cache, q_slots, seq_lens, block_tables, bu
         _ptr(free_stack), _ptr(free_top), int(free_stack.numel()),
         _ptr(freed_blocks), _ptr(num_freed), int(freed_blocks.numel()),
         _ptr(workspace), int(workspace.numel() * workspace.element_size()), _ptr(status),
-        _ptr(global_scores), _ptr(is_compressed))
+        _ptr(global_scores), _ptr(is_compressed), _ptr(window_lse))
 
 
 def _stream(stream):

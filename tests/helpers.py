@@ -90,14 +90,16 @@ def check_band(kept_gpu, s_ref_final, ell, where=""):
     assert not np.any(kept[must_drop]), f"{where}: kept a token below the band"
 
 
-def full_check(w, inp, res, pool=None, strict_select=True, blockwise=False):
-    """Every parity rule of §8(c) on a fully materialised (small) workload."""
+def full_check(w, inp, res, pool=None, strict_select=True, blockwise=False, window_lse_in=None):
+    """Every parity rule of §8(c) on a fully materialised (small) workload. window_lse_in: the
+    normalisers given to a ZPC_F_LSE_INPUT call (NEXT-4), passed to the oracle as well."""
     geo, prm = geometry(w), oparams(w, pool=pool)
     cfg = w.cfg
     R = len(inp["seq"])
     ref = O.compress(geo, prm, inp["k"], inp["v"], inp["q"], inp["slots"], inp["seq"], inp["tables"],
                      inp["budgets"], inp["refs"], inp["stack"], inp["top"], blockwise=blockwise,
-                     free_capacity=len(inp["stack"]), freed_capacity=len(to_host(w.freed)))
+                     free_capacity=len(inp["stack"]), freed_capacity=len(to_host(w.freed)),
+                     window_lse_in=window_lse_in)
     assert res["status"] == ref.status == O.OK, (res["status"], ref.status)
     gpu_kept = {}
     for r in range(R):

@@ -178,3 +178,32 @@ def test_redundancy_sampled_units_vs_oracle(run7b_red, r, l, h):
     kept = np.zeros(T, bool)
     kept[kg] = True
     assert np.all(kept[s_ref > theta + band]) and not np.any(kept[s_ref < theta - band])
+
+
+# ---- NEXT-4 at full size: single-pass scoring (ZPC_F_LSE_INPUT), the bench's --lse-input launch.
+# The normalisers for all 7168 units come from the library's two-pass stage (standing in for the
+# decode kernel); the sampled units are checked against the oracle's OWN exact normalisers, so an
+# error in either pass fails.
+@pytest.fixture(scope="module")
+def run7b_lse():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2603_08743_b200.batch import window_lse_from_two_pass
+    cfg = CONFIGS["qwen7b"]
+    w = generate(cfg, 2603, np.arange(cfg.R))
+    tables0 = w.layout.tables.copy()
+    w.window_lse = window_lse_from_two_pass(w, zipc.ZPC_F_COUNT_MOVES)
+    desc, params = desc_params(w, flags=zipc.ZPC_F_COUNT_MOVES, lse_input=True)
+    zipc.zpc_compress(desc, params, batch_of(w, desc, params))
+    torch.cuda.synchronize()
+    return cfg, w, desc, params, tables0
+
+
+def test_lse_input_structure_full(run7b_lse):
+    test_status_and_structure(run7b_lse)
+    test_kept_lists_all_units(run7b_lse)
+
+
+@pytest.mark.parametrize("r,l,h", SAMPLES)
+def test_lse_input_sampled_units_vs_oracle(run7b_lse, r, l, h):
+    test_sampled_units_vs_oracle(run7b_lse, r, l, h)

@@ -80,6 +80,7 @@ class DeviceWorkload:
     max_seq_len: int = 0
     f_cache: torch.Tensor | None = None          # NEXT-2 global-score pool
     is_compressed: torch.Tensor | None = None    # NEXT-2 [R]
+    window_lse: torch.Tensor | None = None       # NEXT-4 fp32 [L][M][w][h_q] normalisers (ZPC_F_LSE_INPUT)
 
 
 def alloc_outputs(R, L, h_kv, N_total, freed_capacity, device="cuda"):
