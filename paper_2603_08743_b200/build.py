@@ -34,7 +34,10 @@ def _nvcc(srcs, out, includes, extra=()):
 def build_lib():
     csrc = os.path.join(HERE, "csrc")
     srcs = sorted(os.path.join(csrc, f) for f in os.listdir(csrc) if f.endswith(".cu"))
-    return _nvcc(srcs, os.path.join(HERE, "lib", "libzipc.so"), [os.path.join(ROOT, "include"), csrc])
+    # ZPC_EXTRA_NVCC / ZPC_LIB_OUT: an alternative build of the same sources (A/B timing via ZPC_LIB)
+    out = os.environ.get("ZPC_LIB_OUT") or os.path.join(HERE, "lib", "libzipc.so")
+    extra = os.environ.get("ZPC_EXTRA_NVCC", "").split()
+    return _nvcc(srcs, out, [os.path.join(ROOT, "include"), csrc], extra)
 
 
 def build_gen():

@@ -37,7 +37,8 @@ constexpr int kThreads = 512;    // 16 warps: Q-TMA, MMA, (idle), feeder, 4 K lo
 constexpr int kLoadWarps = 4;
 constexpr int kEpiWarp0 = 8;     // first epilogue warp (warps 8..15: lane quarter = warp % 4)
 constexpr bool kPolyOffload = false;   // 25% of pass-1 exp2 on the FMA pipe (pays off only when MUFU-bound)
-constexpr int kIdSlots = 2;      // block ids of the tile being gathered (double-buffered, feeder warp)
+constexpr int kIdSlots = 8;      // block-id ring of the feeder warp (tiles in flight + 2 being read)
+constexpr int kIdAhead = 4;      // tiles whose ids the feeder has in flight ahead of the published one
 constexpr int kMaxIds = 32;      // block ids per 128-token tile (b >= 5)
 constexpr int kEpiWarps = 8;
 // setmaxnreg budget: 8 producer warps x kProdRegs + 8 epilogue warps x kEpiRegs <= 64K registers
@@ -47,6 +48,9 @@ static_assert(8 * kProdRegs + 8 * kEpiRegs <= 2048, "register file: 65536 = 32 l
 constexpr uint32_t kL1Reserve = 0;   // L1 left unallocated (cp.async does not need it: measured)
 constexpr uint32_t kTmemCols = 512;
 constexpr float kLog2e = 1.4426950408889634f;
+#ifndef ZPC_WAIT_HINT_NS
+#define ZPC_WAIT_HINT_NS 1000000   // mbarrier try_wait suspend-time hint (0 = none)
+#endif
 
 // ------------------------------------------------------------------ PTX wrappers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -65,12 +69,20 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   uint32_t done = 0;
   long long spins = 0;
   while (true) {
-    // suspend-time hint: the thread sleeps until the phase completes (or ~1 ms), no busy polling
+#if ZPC_WAIT_HINT_NS > 0
+    // suspend-time hint: the thread sleeps until the phase completes (or the hint), no busy polling
     asm volatile(
         "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
         : "=r"(done)
-        : "r"(bar), "r"(parity), "r"(1000000)
+        : "r"(bar), "r"(parity), "r"(ZPC_WAIT_HINT_NS)
         : "memory");
+#else
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+#endif
     if (done) return;
     if (++spins > (1LL << 22)) __trap();   // a pipeline bug must fail loudly, never hang the GPU
   }
@@ -398,7 +410,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
   const uint32_t xchg0 = smem_u32(bars + 16);
   const uint32_t augf = smem_u32(bars + 18);                  // B_aug of the current unit written
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warp index broadcast from lane 0: the compiler then treats it (and what it guards) as warp-uniform
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const int rank = C > 1 ? (int)(blockIdx.x % C) : 0;
   const int cluster_id = blockIdx.x / C;
   const int nclusters = gridDim.x / C;
@@ -439,7 +452,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
   __syncthreads();
   if (C > 1) cluster_sync_all();        // peers' barriers are initialised before any remote arrive
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);   // warp-uniform TMEM base
   const float scale = kLog2e * rsqrtf((float)D);
 
   // per-unit geometry, identical in every role
@@ -529,7 +542,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
         reinterpret_cast<unsigned long long*>(c.ws.kept)[ld_step * 4 + 0] = gtimer();
       named_bar(4, kLoadWarps * 32 + 32);                     // feeder: ids of this tile, stage free
       // all block ids first (explicit ld.shared: a generic load would queue behind the copies)
-      const uint32_t sid = ids_base + (uint32_t)(ld_step & 1) * kMaxIds * 4;
+      const uint32_t sid = ids_base + (uint32_t)(ld_step % kIdSlots) * kMaxIds * 4;
       if (c.b == 16 && !(c.debug & 256u)) {
         // block-major fast path (b = 16): one id per block, this thread's 16/RPP rows of the block
         // at a constant stride -- few instructions per cp.async (the gather shares its SMSPs with
@@ -583,34 +596,59 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
     while (ld_unit < units) issue_next_load();
 
   } else if (warp == 3 && !(c.debug & 2048u)) {
-    // ================= feeder: for every K tile, in the loaders' order, the block ids (one table
-    // load per lane, issued before the wait so its latency overlaps it) and the stage's release by
-    // the MMA (the empty mbarrier, polled here only); then one named barrier with the 128
-    // gathering threads publishes both. The loaders block in bar.sync instead of polling (their
-    // polls cost issue slots on SMSPs the MUFU-bound epilogue shares; measured). bar.sync on both
-    // sides keeps the feeder from running ahead; ids are double-buffered (slot g & 1 is rewritten
-    // only after every loader has passed barrier g + 1, i.e. finished reading tile g's ids).
-    int f_unit = cluster_id, f_i = 0;
-    UnitInfo f_u = f_unit < units ? unit_info(f_unit) : UnitInfo{};
-    for (int g = 0;; ++g) {
-      while (f_unit < units && f_i >= f_u.p1 + f_u.nt) {
-        f_unit += nclusters;
-        f_i = 0;
-        if (f_unit < units) f_u = unit_info(f_unit);
+    // ================= feeder: for every K tile, in the loaders' order, the block ids and the
+    // stage's release by the MMA (the empty mbarrier, polled here only); then one named barrier
+    // with the 128 gathering threads publishes both. The loaders block in bar.sync instead of
+    // polling (their polls cost issue slots on SMSPs the MUFU-bound epilogue shares; measured).
+    // The ids are copied table -> smem ring by 4-byte cp.async kIdAhead tiles ahead of the one
+    // being published, so the table load latency is off the per-tile critical path (a load issued
+    // per tile right before its publication made every tile wait one L2/DRAM round trip:
+    // measured ~1500 cycles per step with the gather, MMA and epilogue all disabled).
+    // Ring slot (g % kIdSlots) is rewritten at iteration g - kIdAhead, i.e. before barrier
+    // g - kIdAhead; the loaders finished reading tile g - kIdSlots's slot before they reached
+    // barrier g - kIdSlots + 1 <= g - kIdAhead - 1 (kIdSlots >= kIdAhead + 2).
+    static_assert(kIdSlots >= kIdAhead + 2, "id ring too small for the lookahead");
+    int l_unit = cluster_id, l_i = 0;            // load cursor (kIdAhead tiles ahead)
+    UnitInfo l_u = l_unit < units ? unit_info(l_unit) : UnitInfo{};
+    int p_unit = cluster_id, p_i = 0;            // publish cursor
+    UnitInfo p_u = l_u;
+    const uint32_t ids_base = smem_u32(ids);
+    auto issue_ids = [&](int slot) {
+      while (l_unit < units && l_i >= l_u.p1 + l_u.nt) {
+        l_unit += nclusters;
+        l_i = 0;
+        if (l_unit < units) l_u = unit_info(l_unit);
       }
-      if (f_unit >= units) break;
-      const int t0 = tile_of(f_u, f_i) * kTile;
-      const int j0 = t0 / c.b;
-      const int nb = (min(t0 + kTile, f_u.T) - 1) / c.b - j0 + 1;
-      const int v = lane < nb ? __ldg(c.tables + (size_t)f_u.r * c.table_stride + j0 + lane) : 0;
+      if (l_unit < units) {
+        const int t0 = tile_of(l_u, l_i) * kTile;
+        const int j0 = t0 / c.b;
+        const int nb = (min(t0 + kTile, l_u.T) - 1) / c.b - j0 + 1;
+        if (lane < nb)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(ids_base + (uint32_t)(slot * kMaxIds + lane) * 4u),
+                       "l"(c.tables + (size_t)l_u.r * c.table_stride + j0 + lane) : "memory");
+        ++l_i;
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");   // one group per tile (possibly empty)
+    };
+#pragma unroll 1
+    for (int k = 0; k < kIdAhead; ++k) issue_ids(k);
+    for (int g = 0;; ++g) {
+      while (p_unit < units && p_i >= p_u.p1 + p_u.nt) {
+        p_unit += nclusters;
+        p_i = 0;
+        if (p_unit < units) p_u = unit_info(p_unit);
+      }
+      if (p_unit >= units) break;
+      issue_ids((g + kIdAhead) % kIdSlots);
       if (g >= K::ST) {   // stage reuse: the MMAs that read it are complete
         if (lane == 0) mbar_wait(empty0 + 8 * (g % K::ST), ((g / K::ST) & 1) ^ 1);
         __syncwarp();
       }
-      ids[(g & 1) * kMaxIds + lane] = v;
+      asm volatile("cp.async.wait_group %0;" ::"n"(kIdAhead) : "memory");   // tile g's ids landed
       named_bar(4, kLoadWarps * 32 + 32);
-      ++f_i;
+      ++p_i;
     }
+    asm volatile("cp.async.wait_all;" ::: "memory");
   } else if (warp == 1) {
     // ================= MMA issuer: the whole warp runs converged (descriptors are warp-uniform,
     // so ptxas keeps them in uniform registers) and one elected lane issues each tcgen05.mma /
@@ -622,9 +660,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
     const uint64_t aug_b = none_desc(smem_u32(smem + K::OFF_AUG_B), 128, 256);
     const uint64_t qd0 = sw128_desc(smem_u32(smem + K::OFF_Q0));
     for (int it = 0, unit = cluster_id; unit < units; ++it, unit += nclusters) {
-      const UnitInfo u = unit_info(unit);
+      const UnitInfo uu = unit_info(unit);
+      // step counts broadcast from lane 0 so the loop control (and every descriptor) stays in
+      // uniform registers: no R2UR moves around each tcgen05.mma
+      const int p1 = __shfl_sync(0xffffffffu, uu.p1, 0), nsteps = __shfl_sync(0xffffffffu, uu.p1 + uu.nt, 0);
       mbar_wait(qfull0, it & 1);
-      for (int i = 0; i < u.p1 + u.nt; ++i, ++kstep, ++astep) {
+      for (int i = 0; i < nsteps; ++i, ++kstep, ++astep) {
         const int s = kstep % K::ST, a = astep & 1;
         const bool mrec = (c.debug & 1u) && blockIdx.x == 0 && astep < 1024 && lane == 0;
         unsigned long long* mdbg = reinterpret_cast<unsigned long long*>(c.ws.kept);
@@ -632,7 +673,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
         mbar_wait(acce0 + 8 * a, ((astep >> 1) & 1) ^ 1);
         if (mrec) mdbg[16384 + astep * 4 + 1] = gtimer();
         if (!(c.debug & 2048u)) mbar_wait(full0 + 8 * s, (kstep / K::ST) & 1);
-        if (i == u.p1) mbar_wait(augf, it & 1);   // this unit's -L2/s is in B_aug
+        if (i == p1) mbar_wait(augf, it & 1);   // this unit's -L2/s is in B_aug
         if (mrec) mdbg[16384 + astep * 4 + 2] = gtimer();
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // cp.async data -> tensor core
         tc_fence_after();
@@ -641,7 +682,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
         // descriptor start addresses are in 16-B units: a byte offset o adds o >> 4
         if (c.debug & 4u) {
           // debug: no MMA
-        } else if (i < u.p1) {
+        } else if (i < p1) {
 #pragma unroll
           for (int half = 0; half < K::M1H; ++half)
 #pragma unroll

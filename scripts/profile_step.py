@@ -23,11 +23,16 @@ ap.add_argument("--requests", type=int, default=8)
 ap.add_argument("--steps", type=int, default=1)
 ap.add_argument("--cudacore", action="store_true")
 ap.add_argument("--redundancy", action="store_true")
+ap.add_argument("--lse-input", action="store_true", help="NEXT-4 single-pass scoring")
 a = ap.parse_args()
 cfg = CONFIGS[a.config]
 w = generate(cfg, 2603, np.arange(a.requests))
 flags = zipc.ZPC_F_SCORE_CUDACORE if a.cudacore else 0
-desc, params = desc_params(w, flags=flags, redundancy=(0.2, 0.4, 0.8) if a.redundancy else None)
+if a.lse_input:
+    from paper_2603_08743_b200.batch import window_lse_from_two_pass
+    w.window_lse = window_lse_from_two_pass(w, flags)
+desc, params = desc_params(w, flags=flags, redundancy=(0.2, 0.4, 0.8) if a.redundancy else None,
+                           lse_input=a.lse_input)
 b = batch_of(w, desc, params)
 for _ in range(a.steps):
     zipc.zpc_compress(desc, params, b)
