@@ -244,6 +244,10 @@ def main():
                     help="NEXT-4: single-pass scoring with the window normalisers supplied (ZPC_F_LSE_INPUT); "
                          "the normalisers a decode engine would hold are produced untimed by one two-pass "
                          "zpc_score call before the timed steps")
+    ap.add_argument("--wave", type=int, default=0, help="requests per call per GPU (default: the config's)")
+    ap.add_argument("--graph", action="store_true",
+                    help="NEXT-3: replay the whole step as one captured CUDA graph (launch-bound small batches); "
+                         "value/ms_per_step then come from the graph replays, stage_ms from the eager steps")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -252,12 +256,13 @@ def main():
 
     from zpc_inputs import CONFIGS
     cfg = CONFIGS[args.config]
-    per_gpu = cfg.wave or cfg.R
+    per_gpu = args.wave or cfg.wave or cfg.R
     workload = (f"{cfg.name}: {per_gpu} req/GPU x {cfg.seq_lens[0]} tok, L={cfg.L} h_kv={cfg.h_kv} h_q={cfg.h_q} "
                 f"d={cfg.d} b={cfg.b} w={cfg.w} N_max={cfg.n_max} budget={cfg.budget} pool={cfg.pool_kernel}"
                 + (f" prefix={cfg.prefix_tokens}" if cfg.prefix_tokens else "")
                 + (" + NEXT-1 lightning redundancy (lambda=0.2 tau=0.4 p=0.8)" if args.redundancy else "")
-                + (" + NEXT-4 window LSE input (single-pass score)" if args.lse_input else ""))
+                + (" + NEXT-4 window LSE input (single-pass score)" if args.lse_input else "")
+                + (" [CUDA graph]" if args.graph else ""))
 
     if args.impl == "reference":
         if rank != 0:
@@ -365,6 +370,30 @@ def main():
         for i in range(len(stages)):
             stage_ms[i] += evs[i].elapsed_time(evs[i + 1])
     step_ms_total = float(stage_ms.sum())
+    eager_ms = step_ms_total
+    graph_info = None
+    if args.graph:
+        # the same stage sequence captured once; restores stay outside the graph (untimed)
+        g = torch.cuda.CUDAGraph()
+        restore()
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g):
+            cap = torch.cuda.current_stream()
+            for fn in stages:
+                fn(desc, params, batch, cap)
+        g_ms = 0.0
+        for i in range(max(3, args.warmup) + args.steps):
+            restore()
+            a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            g.replay()
+            b_.record(stream)
+            b_.synchronize()
+            if i >= max(3, args.warmup):
+                g_ms += a.elapsed_time(b_)
+        assert int(w.status.item()) == 0, zipc.status_string(int(w.status.item()))
+        step_ms_total = g_ms
+        graph_info = {"graph_ms_per_step": g_ms / args.steps, "eager_ms_per_step": eager_ms / args.steps}
     max_ms = max_over_ranks(step_ms_total, dist, dev)
     R_all = per_gpu * world
     ms_per_step = max_ms / args.steps
@@ -396,6 +425,7 @@ def main():
                                                         stage_ms[stage_names.index("redundancy")] / args.steps,
                                                         peaks)} if args.redundancy else {}),
         "kv_tokens_per_s": T_sum * world / (ms_per_step / 1e3),
+        **({"cuda_graph": graph_info} if graph_info else {}),
         "wall_s_incl_restores": wall,
     }
 

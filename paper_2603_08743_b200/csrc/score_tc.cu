@@ -335,7 +335,7 @@ struct Cfg {
   static constexpr uint32_t OFF_BAR = OFF_IDS + kIdSlots * kMaxIds * 4;
   static constexpr uint32_t SMEM = OFF_BAR + 56 * 8 + 16 + 1024;     // + alignment slack
   static_assert(GW % 16 == 0 && GW <= 256, "pass-2 UMMA N must be a multiple of 16, <= 256");
-  static_assert(W == 32, "epilogue batching assumes w = 32");
+  static_assert(W == 32 || W == 16, "epilogue batching assumes w = 32 (configs) or 16 (the paper's, PAPER.md:162)");
   static_assert(ST >= 2, "K ring needs >= 2 stages");
   static_assert(Q_BYTES % 1024 == 0, "Q slabs must stay 1024-B aligned for SW128");
 };
@@ -1005,16 +1005,27 @@ int cluster_size(const Call& c) {
 
 template <int G, int W, int D>
 cudaError_t launch_c(const Call& c, const CUtensorMap& tq, cudaStream_t s) {
+#ifdef ZPC_SCORE_BIG_CLUSTERS   // tuning builds only: 4- and 8-CTA clusters measured slower
   switch (cluster_size(c)) {
     case 8: return launch_tc<G, W, D, 8>(c, tq, s);
     case 4: return launch_tc<G, W, D, 4>(c, tq, s);
-    case 2: return launch_tc<G, W, D, 2>(c, tq, s);
-    default: return launch_tc<G, W, D, 1>(c, tq, s);
+    default: break;
   }
+#endif
+  return cluster_size(c) >= 2 ? launch_tc<G, W, D, 2>(c, tq, s) : launch_tc<G, W, D, 1>(c, tq, s);
 }
 
 template <int D>
 cudaError_t dispatch_g(const Call& c, const CUtensorMap& tq, cudaStream_t s, bool* used) {
+  if (c.w == 16 && D == 128) {
+    // the paper's own operating point (w = 16): Qwen3-8B / DS-Llama-8B (G = 4), 32B (G = 8)
+    *used = true;
+    switch (c.G) {
+      case 4: return launch_c<4, 16, D>(c, tq, s);
+      case 8: return launch_c<8, 16, D>(c, tq, s);
+      default: *used = false; return cudaSuccess;
+    }
+  }
   if (c.w != 32) return cudaSuccess;
   *used = true;
   switch (c.G) {

@@ -77,19 +77,21 @@ def test_kept_lists_all_units(run7b):
     assert bool((last == torch.arange(T - cfg.w, T, device=kept.device)[None, :]).all())
 
 
-@pytest.mark.parametrize("r,l,h", SAMPLES)
-def test_sampled_units_vs_oracle(run7b, r, l, h):
-    cfg, w, desc, params, tables0 = run7b
-    T = 8192
-    seed = 2603
+def check_sampled_unit(cfg, w, desc, params, tables0, r, l, h, seed=2603):
+    """One unit of a device-generated batch (global request id r = batch index r) against the oracle:
+    scores, band rule, strict select, and the moved K/V bytes in the target blocks."""
+    T = int(w.layout.seq_lens[r])
     # host regeneration of this unit's inputs (logical order), independent of the GPU generator
     kt = k_rows(cfg, seed, r, l, h, np.arange(T), T)                 # bf16 bits [T, d]
     q = q_rows(cfg, seed, r, l)                                       # [w, h_q, d]
-    geo = O.Geometry(L=1, h_kv=1, h_q=cfg.G, d=cfg.d, b=cfg.b, N_total=T // cfg.b, M=1, w=cfg.w, dtype="bf16")
-    kf = O.widen(kt, "bf16").reshape(T // cfg.b, cfg.b, 1, cfg.d)
+    N = -(-T // cfg.b)
+    kpad = np.zeros((N * cfg.b, cfg.d), kt.dtype)
+    kpad[:T] = kt
+    geo = O.Geometry(L=1, h_kv=1, h_q=cfg.G, d=cfg.d, b=cfg.b, N_total=N, M=1, w=cfg.w, dtype="bf16")
+    kf = O.widen(kpad, "bf16").reshape(N, cfg.b, 1, cfg.d)
     qf = O.widen(q[:, h * cfg.G:(h + 1) * cfg.G, :], "bf16")
-    s_ref = O.attention_scores(O.logits_dense(geo, qf, kf, np.arange(T // cfg.b), T, 0), T)
-    R = cfg.R
+    s_ref = O.attention_scores(O.logits_dense(geo, qf, kf, np.arange(N), T, 0), T)
+    R = len(w.layout.seq_lens)
     units = R * cfg.L * cfg.h_kv
     lay = zipc.zpc_workspace_layout_get(desc, params, R)
     u = (r * cfg.L + l) * cfg.h_kv + h
@@ -110,6 +112,11 @@ def test_sampled_units_vs_oracle(run7b, r, l, h):
     v_now = w.v[l][blk, slot, h].cpu().numpy().view(np.uint16)
     np.testing.assert_array_equal(k_now, kt[kept])
     np.testing.assert_array_equal(v_now, vt)
+
+
+@pytest.mark.parametrize("r,l,h", SAMPLES)
+def test_sampled_units_vs_oracle(run7b, r, l, h):
+    check_sampled_unit(*run7b, r, l, h)
 
 
 # ---- NEXT-1 at full size: the bench's launch configuration with ZPC_F_REDUNDANCY
@@ -207,3 +214,39 @@ def test_lse_input_structure_full(run7b_lse):
 @pytest.mark.parametrize("r,l,h", SAMPLES)
 def test_lse_input_sampled_units_vs_oracle(run7b_lse, r, l, h):
     test_sampled_units_vs_oracle(run7b_lse, r, l, h)
+
+
+# ---- NEXT-3: the paper's operating point at the bench's exact launch (4 requests x T = 2304,
+# Qwen3-8B shape, b = 256, w = 16, N_max = 9; tcgen05 w = 16 path)
+@pytest.fixture(scope="module")
+def run_paper_op():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    cfg = CONFIGS["paper_op"]
+    w = generate(cfg, 2603, np.arange(cfg.wave))
+    tables0 = w.layout.tables.copy()
+    desc, params = desc_params(w, flags=zipc.ZPC_F_COUNT_MOVES)
+    zipc.zpc_compress(desc, params, batch_of(w, desc, params))
+    torch.cuda.synchronize()
+    return cfg, w, desc, params, tables0
+
+
+def test_paper_op_structure(run_paper_op):
+    cfg, w, desc, params, tables0 = run_paper_op
+    assert int(w.status.item()) == 0
+    T, nm = 2304, cfg.n_max
+    np.testing.assert_array_equal(w.new_lens.cpu().numpy(), np.minimum(T, w.budgets_host))
+    tables = w.tables.cpu().numpy()
+    np.testing.assert_array_equal(tables[:, :nm], tables0[:, :nm])
+    assert int(w.num_freed.item()) == 0          # N = N_max: exactly one block's worth evicted, none freed
+    R = cfg.wave
+    units = R * cfg.L * cfg.h_kv
+    lay = zipc.zpc_workspace_layout_get(desc, params, R)
+    kept = workspace_view(w, desc, params, "kept", torch.int32, (units, lay.kept_stride))
+    last = kept[:, 2048 - cfg.w:2048]
+    assert bool((last == torch.arange(T - cfg.w, T, device=kept.device)[None, :]).all())
+
+
+@pytest.mark.parametrize("r,l,h", [(0, 0, 0), (1, 17, 5), (3, 35, 7), (2, 8, 2)])
+def test_paper_op_sampled_units_vs_oracle(run_paper_op, r, l, h):
+    check_sampled_unit(*run_paper_op, r, l, h)

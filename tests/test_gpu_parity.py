@@ -74,6 +74,20 @@ def test_prefix_small(cuda_ok):
         _run(cfg, seed=6)
 
 
+@pytest.mark.parametrize("flags", [0, zipc.ZPC_F_SCORE_CUDACORE])
+def test_paper_operating_point_shape(cuda_ok, flags):
+    """NEXT-3: b = 256, w = 16, N_max = 9 with the Qwen3-8B head shape (G = 4), ragged T
+    around the steady state N_max * b (one partial block, one freed block)."""
+    cfg = scaled(CONFIGS["paper_op"], L=2, h_kv=2, h_q=8, seq_lens=[2304, 2100, 2500], wave=0, free_slack=3)
+    _run(cfg, seed=8, flags=flags)
+
+
+def test_paper_operating_point_g8(cuda_ok):
+    """w = 16 with G = 8 (Qwen3-32B-like head ratio), tcgen05 path."""
+    cfg = scaled(CONFIGS["paper_op"], L=1, h_kv=2, h_q=16, seq_lens=[2304, 2049], wave=0, free_slack=3)
+    _run(cfg, seed=9)
+
+
 def test_edge_min_trigger_and_w_gt_b(cuda_ok):
     """N == N_max exactly, partial last block, w > b, budget == w."""
     cfg = scaled(CONFIGS["qwen7b"], L=1, h_kv=1, h_q=7, n_max=3, seq_lens=[33, 48, 40], budget=32, free_slack=2)

@@ -79,6 +79,12 @@ def _cfgs():
         "prefix": Config("prefix", L=28, h_kv=4, h_q=28, d=128, b=16, dtype="bf16", w=32, n_max=129,
                          pool_kernel=7, seq_lens=[4096 + 8192] * 1024, budget=2048, prefix_tokens=4096,
                          wave=128),
+        # NEXT-3: the paper's operating point (b = 256, w = 16; budget 2048 -> N_max = 9),
+        # Qwen3-8B shape (L = 36, h_kv = 8, h_q = 32, d = 128 from the public model config), steady
+        # state T = N_max * b (exactly one block evicted per call), ~1/b of the running requests per call
+        # (PAPER.md:153): 4 requests per call per GPU
+        "paper_op": Config("paper_op", L=36, h_kv=8, h_q=32, d=128, b=256, dtype="bf16", w=16, n_max=9,
+                           pool_kernel=7, seq_lens=[2304] * 64, budget=2048, wave=4, free_slack=4),
     }
 
 
