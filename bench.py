@@ -180,13 +180,15 @@ def max_over_ranks(value, dist=None, device=None):
 TRAFFIC_FILE = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_traffic.json")
 
 
-def measured_traffic(cfg, per_gpu):
+def measured_traffic(cfg, per_gpu, lse_input=False):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu --set full capture
-    of this exact workload (profiles/r01_traffic.json: the full qwen7b batch, 64 requests), else {}."""
-    if cfg.name != "qwen7b" or per_gpu != 64 or not os.path.exists(TRAFFIC_FILE):
+    of this exact workload (profiles/r01_traffic.json: the full qwen7b batch, 64 requests;
+    profiles/r01_traffic_lse.json: the same with --lse-input), else {}."""
+    path = TRAFFIC_FILE.replace(".json", "_lse.json") if lse_input else TRAFFIC_FILE
+    if cfg.name != "qwen7b" or per_gpu != 64 or not os.path.exists(path):
         return {}
     try:
-        kern = json.load(open(TRAFFIC_FILE))["kernels"]
+        kern = json.load(open(path))["kernels"]
     except (OSError, ValueError, KeyError):
         return {}
     out = {}
@@ -405,7 +407,7 @@ def main():
     score_ms = stage_ms[stage_names.index("score")] / args.steps
     compact_ms = stage_ms[stage_names.index("compact")] / args.steps
     step_bytes = ab["score"] + ab["select"] + ab["compact"]
-    traffic = {} if args.lse_input else measured_traffic(cfg, per_gpu)
+    traffic = measured_traffic(cfg, per_gpu, args.lse_input)
     roofline = {"kernel": "score (a1+a2)", "bound": "hbm", "achieved": ab["score"] / (score_ms / 1e3) / 1e9,
                 "peak": peaks["hbm"], "unit": "GB/s", "peak_src": peaks["src"],
                 "traffic": traffic.get("score"), "traffic_unit": "bytes/launch (dram read+write, ncu --set full)",
