@@ -194,7 +194,7 @@ def measured_traffic(cfg, per_gpu, lse_input=False):
     out = {}
     for name, rec in kern.items():
         tot = rec["dram_bytes_read"] + rec["dram_bytes_write"]
-        if f"k_score_tc<{cfg.h_q // cfg.h_kv}, {cfg.w}, {cfg.d}," in name:
+        if any(f"{k}<{cfg.h_q // cfg.h_kv}, {cfg.w}, {cfg.d}" in name for k in ("k_score_tc", "k_score_ovl", "k_score_pair")):
             out["score"] = tot
         elif "k_compact" in name:
             out["compact"] = tot

@@ -187,3 +187,20 @@ def test_deterministic(cuda_ok):
         o["stack"] = o["stack"][:o["top"]]
     for key in ("S", "kept", "k", "v", "tables", "freed", "stack", "new_lens"):
         np.testing.assert_array_equal(outs[0][key], outs[1][key])
+
+
+# Several units per persistent CTA cluster (192 units > the 74 clusters of a B200), so the overlapped
+# schedule interleaves pass 1 of one unit with pass 2 of the previous one on every cluster, with ragged
+# lengths (partial last tiles, a unit whose 256-token pair tile is half empty). Each scoring kernel
+# variant is selected through its launch-time switch (ZPC_SCORE_OVL / ZPC_SCORE_PAIR, read per launch).
+@pytest.mark.parametrize("variant", ["ovl", "pair", "serial"])
+@pytest.mark.parametrize("shape", [("qwen7b", 7), ("qwen32b", 5), ("llama8b", 4), ("llama8b", 8)])
+def test_many_units_per_cluster(cuda_ok, monkeypatch, variant, shape):
+    name, G = shape
+    if variant == "pair" and G not in (7, 8):
+        pytest.skip("the CTA-pair kernel covers G*w/2 >= 112 columns per CTA (G = 7, 8)")
+    monkeypatch.setenv("ZPC_SCORE_OVL", "0" if variant == "serial" else "1")
+    monkeypatch.setenv("ZPC_SCORE_PAIR", "1" if variant == "pair" else "0")
+    cfg = scaled(CONFIGS[name], L=4, h_kv=8, h_q=8 * G, n_max=9,
+                 seq_lens=[300, 1100, 144, 700, 385, 896], budget=(32, 128), wave=0, free_slack=6)
+    _run(cfg, seed=11 + G)
