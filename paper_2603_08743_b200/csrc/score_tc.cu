@@ -1022,7 +1022,7 @@ struct CfgO {
   static constexpr uint32_t OFF_AUG_A = 2 * Q_BYTES;
   static constexpr uint32_t OFF_AUG_B = OFF_AUG_A + AUG_A_BYTES;
   static constexpr uint32_t AUG_END = (OFF_AUG_B + AUG_B_BYTES + 1023) / 1024 * 1024;
-  static constexpr uint32_t F_BYTES = (4 * GW + 2 * kTile) * 4;   // pmv[2][GW], psv[2][GW], comb[2][kTile]
+  static constexpr uint32_t F_BYTES = (4 * GW + 2 * kTile + 2 * 128) * 4;   // pmv[2][GW], psv[2][GW], comb[2][kTile], pmh[2][128]
   static constexpr uint32_t IDS_BYTES = kIdSlots * kMaxIds * 4;
   static constexpr uint32_t BAR_BYTES = 40 * 8 + 16;
   static constexpr uint32_t MISC = F_BYTES + IDS_BYTES + BAR_BYTES;
@@ -1294,13 +1294,21 @@ __global__ void __launch_bounds__(kThreadsO, 1) k_score_ovl(Call c, const __grid
               // pass 1: two 64-token sub-steps, each into its own double-buffered accumulator, so the
               // epilogue frees a buffer right after loading it (N = 64; B = rows 64*hs.. of the stage)
 #pragma unroll 1
-              for (int hs = 0; hs < 2; ++hs, ++n1) {
+              for (int hs = 0; hs < (K::M1H == 1 ? 1 : 2); ++hs, ++n1) {
                 const int a = n1 & 1;
                 mbar_wait(acce0 + 8 * a, ((n1 >> 1) & 1) ^ 1);
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 tc_fence_after();
                 const uint32_t dacc = tmem + a * 128;
-                if (!(c.debug & 4u)) {
+                if (K::M1H == 1) {
+                  // one M-half: the whole 128-token tile in one sub-step (N = 128, 128 columns)
+                  if (!(c.debug & 4u)) {
+#pragma unroll
+                    for (int kk = 0; kk < K::KSTEPS; ++kk)
+                      umma_elect(dacc, qdA + (((kk >> 2) * K::SLAB_Q + (kk & 3) * 32) >> 4),
+                                 kd0 + (((kk >> 2) * K::SLAB_K + (kk & 3) * 32) >> 4), idesc_bf16(128, kTile), kk > 0);
+                  }
+                } else if (!(c.debug & 4u)) {
 #pragma unroll
                   for (int half = 0; half < K::M1H; ++half)
 #pragma unroll
@@ -1344,9 +1352,15 @@ __global__ void __launch_bounds__(kThreadsO, 1) k_score_ovl(Call c, const __grid
     const int q = warp & 3;
     const int half = ew >> 2;
     const int col = half * 128 + q * 32 + lane;
-    const bool warp_cols = (half * 128 + q * 32) < K::GW;
     const bool col_ok = col < K::GW;
-    const int u1 = col_ok ? col / G : 0;
+    // G*w <= 128 (one M-half): the two warps of a quarter share the columns and split each tile's
+    // tokens (64 each, one N = 128 MMA per tile) instead of leaving the second warp idle
+    constexpr bool kSplit = K::M1H == 1;
+    constexpr int kSub = kSplit ? 1 : 2;           // pass-1 sub-steps (accumulator buffers) per tile
+    const int pcol = kSplit ? q * 32 + lane : col;  // this thread's column in pass 1
+    const bool warp_cols = (kSplit ? q * 32 : half * 128 + q * 32) < K::GW;
+    const int u1 = pcol < K::GW ? pcol / G : 0;
+    float* pmh = comb + 2 * kTile;                  // [2][128] split-half merge (m, s)
     const uint32_t tbase0 = tmem + ((uint32_t)(q * 32) << 16) + half * 64;   // + 128 * buffer
     auto write_aug = [&](int cc, float L2) {
       const float nv = -L2 / scale;
@@ -1367,7 +1381,7 @@ __global__ void __launch_bounds__(kThreadsO, 1) k_score_ovl(Call c, const __grid
       float m = -INFINITY, ssum = 0.f, m1 = -INFINITY, s1 = 0.f;
       for (int k = 0; k < A.nt; ++k) {
         if (c.debug & 2u) {   // bisection: no epilogue math
-          for (int hs = 0; hs < 2; ++hs, ++n1) {
+          for (int hs = 0; hs < kSub; ++hs, ++n1) {
             mbar_wait(accf0 + 8 * (n1 & 1), (n1 >> 1) & 1);
             __syncwarp();
             if (lane == 0) mbar_arrive(acce0 + 8 * (n1 & 1));
@@ -1408,7 +1422,7 @@ __global__ void __launch_bounds__(kThreadsO, 1) k_score_ovl(Call c, const __grid
           __syncwarp();
           if (lane == 0) mbar_arrive(acce0 + 8 * a);
           if constexpr (kMask) {
-            const int tb = t0 + bp * 2 * NB;
+            const int tb = t0 + (kSplit ? half : bp) * 2 * NB;
 #pragma unroll
             for (int jj = 0; jj < 2 * NB; ++jj) vp[jj] = (tb + jj > limit1) ? -INFINITY : vp[jj];
           }
@@ -1416,7 +1430,7 @@ __global__ void __launch_bounds__(kThreadsO, 1) k_score_ovl(Call c, const __grid
           online(vp + NB, m1, s1);
         };
         if (!warp_cols) {
-          for (int hs = 0; hs < 2; ++hs, ++n1) {
+          for (int hs = 0; hs < kSub; ++hs, ++n1) {
             mbar_wait(accf0 + 8 * (n1 & 1), (n1 >> 1) & 1);
             tc_fence_after();
             tc_fence_before();
@@ -1425,10 +1439,10 @@ __global__ void __launch_bounds__(kThreadsO, 1) k_score_ovl(Call c, const __grid
           }
         } else if (!need_mask) {
 #pragma unroll 1
-          for (int bp = 0; bp < kTile / (2 * NB); ++bp) pair(bp, std::false_type{});
+          for (int bp = 0; bp < kSub; ++bp) pair(bp, std::false_type{});
         } else {
 #pragma unroll 1
-          for (int bp = 0; bp < kTile / (2 * NB); ++bp) pair(bp, std::true_type{});
+          for (int bp = 0; bp < kSub; ++bp) pair(bp, std::true_type{});
         }
       }
       // ---- end of unit A's pass 1: LSE per column (cluster-combined), into B_aug once the previous
@@ -1438,6 +1452,17 @@ __global__ void __launch_bounds__(kThreadsO, 1) k_score_ovl(Call c, const __grid
         const float mr = mm > -INFINITY ? mm : 0.f;
         ssum = ssum * ex2f(m - mr) + s1 * ex2f(m1 - mr);
         m = mm;
+      }
+      if constexpr (kSplit) {   // fold the second token half into the first warp of the quarter
+        if (half == 1) { pmh[q * 32 + lane] = m; pmh[128 + q * 32 + lane] = ssum; }
+        named_bar(1, 8 * 32);
+        if (half == 0) {
+          const float mo = pmh[q * 32 + lane], so = pmh[128 + q * 32 + lane];
+          const float mm = fmaxf(m, mo);
+          const float mr = mm > -INFINITY ? mm : 0.f;
+          ssum = ssum * ex2f(m - mr) + so * ex2f(mo - mr);
+          m = mm;
+        }
       }
       float L2 = 0.f;
       if (C == 1) {
