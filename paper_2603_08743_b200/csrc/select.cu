@@ -418,20 +418,22 @@ __global__ void __launch_bounds__(NT) k_select_reg(Call c) {
 cudaError_t launch_select(const Call& c, cudaStream_t s) {
   const int units = c.R * c.L * c.h_kv;
   if (units == 0) return cudaSuccess;
-  // register-resident variant while a thread's chunk fits CH <= 32 keys (ZPC_SELECT_REG=0: k_select)
+  // register-resident variant while a thread's chunk fits CH <= 32 keys. ZPC_SELECT_REG (tests and A/B
+  // runs): 0 = always k_select, 2 = k_select_reg for every T <= 32K, unset/1 = by T as below
   const char* e = getenv("ZPC_SELECT_REG");
-  const bool reg = !(e && atoi(e) == 0);
+  const int mode = e ? atoi(e) : 1;
+  const bool reg = mode != 0;
   const int T = c.max_seq_len;
-  if (reg && T <= 32 * kThreads) {
+  // T <= 4K (the paper's operating point, T = 2304): k_select measured faster (0.066 ms per 4-request
+  // call vs 0.078 with 1024 x 4 register keys and 0.114 with 256 x 32)
+  if (reg && (T > 4 * kThreads || mode == 2) && T <= 32 * kThreads) {
     const size_t smem = sizeof(float) * (size_t)(T + T / 32 + 1);
     auto launch = [&](auto kern, int nt) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       kern<<<units, nt, smem, s>>>(c);
       return cudaGetLastError();
     };
-    // 32 keys per thread; the CTA shrinks with T so short units run several CTAs per SM
-    if (T <= 4 * 256) return launch(k_select_reg<256, 4>, 256);
-    if (T <= 8 * 256) return launch(k_select_reg<256, 8>, 256);
+    // 32 keys per thread and a CTA that shrinks with T, so 8K units run 3 CTAs per SM
     if (T <= 32 * 256) return launch(k_select_reg<256, 32>, 256);
     if (T <= 32 * 512) return launch(k_select_reg<512, 32>, 512);
     return launch(k_select_reg<1024, 32>, 1024);

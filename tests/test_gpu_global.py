@@ -21,6 +21,13 @@ from helpers import check_band, check_scores, geometry, gpu_results, snapshot_in
 
 pytestmark = pytest.mark.gpu
 
+
+@pytest.fixture(autouse=True, params=["select_auto", "select_reg"])
+def _select_path(request, monkeypatch):
+    """Run every case through both selection kernels: k_select (what these small T get by default)
+    and the register-resident k_select_reg (ZPC_SELECT_REG=2 forces it for T <= 32K)."""
+    monkeypatch.setenv("ZPC_SELECT_REG", "2" if request.param == "select_reg" else "1")
+
 ALPHA = 0.8
 CASES = {
     "bf16_7b": scaled(CONFIGS["qwen7b"], L=2, h_kv=2, h_q=14, n_max=9, seq_lens=[300, 257, 416, 129 + 128],

@@ -204,3 +204,13 @@ def test_many_units_per_cluster(cuda_ok, monkeypatch, variant, shape):
     cfg = scaled(CONFIGS[name], L=4, h_kv=8, h_q=8 * G, n_max=9,
                  seq_lens=[300, 1100, 144, 700, 385, 896], budget=(32, 128), wave=0, free_slack=6)
     _run(cfg, seed=11 + G)
+
+
+# k_select_reg at every thread-count instance: the dispatch follows the host bound max_seq_len, so small
+# ragged units run through the 256 x 32 / 512 x 32 / 1024 x 32 variants (and k_select for comparison)
+@pytest.mark.parametrize("max_seq_len,mode", [(2048, "2"), (8192, "1"), (16384, "1"), (32768, "1"), (8192, "0")])
+def test_select_kernels(cuda_ok, monkeypatch, max_seq_len, mode):
+    monkeypatch.setenv("ZPC_SELECT_REG", mode)
+    cfg = scaled(CONFIGS["qwen7b"], L=2, h_kv=4, h_q=28, n_max=9, seq_lens=[300, 1100, 144, 700, 385],
+                 budget=(32, 128), wave=0, free_slack=6, pool_kernel=7)
+    _run(cfg, seed=21, max_seq_len=max_seq_len)
