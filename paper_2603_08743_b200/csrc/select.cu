@@ -321,21 +321,45 @@ __global__ void __launch_bounds__(NT) k_select_reg(Call c) {
   // pool (+ redundancy) + pin of this thread's chunk [t0, t0 + CH) -> keys in registers
   const int t0 = threadIdx.x * CH;
   uint32_t key[CH];
+  if (half == 3) {
+    // k_p = 7 (the configs' pool): the chunk and its 3 neighbours on each side are loaded once
+    // (out-of-range = -inf, PAPER.md:482 reading R6), then max over e[i..i+6] by a 2-4-7 doubling tree
+    // (max is exact, so the result is bit-identical to the direct loop below)
+    float e[CH + 6];
 #pragma unroll
-  for (int i = 0; i < CH; ++i) {
-    const int t = t0 + i;
-    float v = 0.f;
-    if (t < T) {
-      if (t >= T - c.w) {
-        v = __int_as_float(0x7f800000);            // +inf: the observation window is always kept
-      } else {
-        v = sS[pidx(t)];
-        const int lo = max(0, t - half), hi = min(T - 1, t + half);
-        for (int j = lo; j <= hi; ++j) v = fmaxf(v, sS[pidx(j)]);
-        if (red) v -= rscale * expf((rr[t] - rmax) * inv_tau);
-      }
+    for (int i = 0; i < CH + 6; ++i) {
+      const int t = t0 - 3 + i;
+      e[i] = (t >= 0 && t < T) ? sS[pidx(t)] : -INFINITY;
     }
-    key[i] = t < T ? orderable(v) : 0u;            // 0 = below every real key; never selected (ell <= T)
+#pragma unroll
+    for (int i = 0; i < CH + 5; ++i) e[i] = fmaxf(e[i], e[i + 1]);       // e[i..i+1]
+#pragma unroll
+    for (int i = 0; i < CH + 3; ++i) e[i] = fmaxf(e[i], e[i + 2]);       // e[i..i+3]
+#pragma unroll
+    for (int i = 0; i < CH; ++i) {
+      const int t = t0 + i;
+      float v = fmaxf(e[i], e[i + 3]);                                    // e[i..i+6] = t-3..t+3
+      if (t >= T - c.w) v = __int_as_float(0x7f800000);  // +inf: the observation window is always kept
+      else if (red) v -= rscale * expf((rr[t] - rmax) * inv_tau);
+      key[i] = t < T ? orderable(v) : 0u;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < CH; ++i) {
+      const int t = t0 + i;
+      float v = 0.f;
+      if (t < T) {
+        if (t >= T - c.w) {
+          v = __int_as_float(0x7f800000);            // +inf: the observation window is always kept
+        } else {
+          v = sS[pidx(t)];
+          const int lo = max(0, t - half), hi = min(T - 1, t + half);
+          for (int j = lo; j <= hi; ++j) v = fmaxf(v, sS[pidx(j)]);
+          if (red) v -= rscale * expf((rr[t] - rmax) * inv_tau);
+        }
+      }
+      key[i] = t < T ? orderable(v) : 0u;            // 0 = below every real key; never selected (ell <= T)
+    }
   }
 
   // MSB radix select of the ell-th largest key (as k_select)

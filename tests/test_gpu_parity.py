@@ -214,3 +214,13 @@ def test_select_kernels(cuda_ok, monkeypatch, max_seq_len, mode):
     cfg = scaled(CONFIGS["qwen7b"], L=2, h_kv=4, h_q=28, n_max=9, seq_lens=[300, 1100, 144, 700, 385],
                  budget=(32, 128), wave=0, free_slack=6, pool_kernel=7)
     _run(cfg, seed=21, max_seq_len=max_seq_len)
+
+
+# k_select_reg's pooling has a register doubling tree for k_p = 7 and the direct loop for every other
+# k_p: the other widths through the register kernel too (strict selection pins the pooled keys)
+@pytest.mark.parametrize("pool", [1, 3, 5, 9])
+def test_select_reg_other_pools(cuda_ok, monkeypatch, pool):
+    monkeypatch.setenv("ZPC_SELECT_REG", "2")
+    cfg = scaled(CONFIGS["qwen7b"], L=1, h_kv=4, h_q=28, n_max=9, seq_lens=[300, 1100, 144, 385],
+                 budget=(32, 128), wave=0, free_slack=6, pool_kernel=pool)
+    _run(cfg, seed=23, pool=pool, max_seq_len=2048)
