@@ -207,9 +207,18 @@ def redundancy_roofline(cfg, seq_lens, world, red_ms, peaks):
     T = np.asarray(seq_lens, np.int64)
     byts = int((T * cfg.d * e + 4 * T).sum() * cfg.L * cfg.h_kv)
     ach = byts / (red_ms / 1e3) / 1e9 if red_ms else None
-    return {"kernel": "k_red_mma" if (cfg.dtype == "bf16" and cfg.b == 16) else "k_red_generic", "bound": "hbm",
+    if cfg.dtype == "bf16" and cfg.b == 16:
+        kern = "k_red_mma"
+    elif cfg.dtype == "bf16" and cfg.b % 16 == 0 and 16 < cfg.b <= 256:
+        kern = "k_red_tile"
+    else:
+        kern = "k_red_generic"
+    # the within-block Gram matrices: b x b x d multiply-adds per block
+    flops = int(2 * cfg.b * cfg.d * (-(-T // cfg.b) * cfg.b).sum() * cfg.L * cfg.h_kv)
+    return {"kernel": kern, "bound": "hbm",
             "achieved": ach, "peak": peaks["hbm"], "unit": "GB/s", "frac": ach / peaks["hbm"] if ach else None,
-            "algorithmic_bytes_per_launch": byts, "ms": red_ms}
+            "algorithmic_bytes_per_launch": byts, "ms": red_ms,
+            "gram_tflops": flops / (red_ms / 1e3) / 1e12 if red_ms else None}
 
 
 # ---------------------------------------------------------------- GPU arm

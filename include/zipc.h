@@ -52,7 +52,8 @@ extern "C" {
                                        unsupported head_dim/dtype, h_q not a multiple of h_kv,
                                        G*w > 256, max_seq_len above the select limit, NULL pointer,
                                        ZPC_F_REDUNDANCY with lambda < 0, tau <= 0, p outside [0,1],
-                                       a non-finite value or block_size > 32, ZPC_F_GLOBAL_SCORE
+                                       a non-finite value, or block_size > 32 unless bf16 with
+                                       block_size a multiple of 16 up to 256, ZPC_F_GLOBAL_SCORE
                                        with alpha outside [0,1] or a NULL global_scores /
                                        is_compressed, ZPC_F_LSE_INPUT with a NULL window_lse */
 #define ZPC_ERR_WORKSPACE      -2   /* workspace_bytes < zpc_workspace_bytes(...) */

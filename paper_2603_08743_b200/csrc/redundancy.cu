@@ -10,6 +10,15 @@
 // mma.sync.m16n8k16 (bf16 -> fp32): one ldmatrix.x4 per K-step yields the A fragment and, because
 // B is the block's own rows, both B fragments (n-tile 0 = {a0, a2}, n-tile 1 = {a1, a3}).
 // k_red_generic (any dtype, b <= 32): one lane per row, fp32 dot products from L1; small/test shapes.
+// k_red_tile (bf16, b = 32..256 in steps of 16, e.g. the paper's b = 256): one 256-thread CTA per
+// block. The b rows are staged once in shared memory by cp.async (rows >= T zero-filled), each warp
+// forms a pair of 16-row stripes of the b x b Gram matrix with ldmatrix + mma.sync.m16n8k16 (A
+// fragments of both stripes held in registers across all column chunks, so each B fragment feeds
+// four MMAs), and a single pass yields both results: the
+// row sums of C over every column j != i, and per column the last row above p together with its
+// value, packed (row + 1) << 32 | value into one 64-bit shared atomicMax (rows are unique within a
+// column, so the maximum carries the value of the largest row). The zeroed entries are subtracted
+// afterwards in ascending column order by the row's own thread (deterministic).
 #include "internal.h"
 
 namespace zpc {
@@ -184,6 +193,185 @@ __global__ void __launch_bounds__(kWarps * 32) k_red_generic(Call c) {
   }
 }
 
+constexpr int kTileThreads = 256;
+
+template <int D>
+__host__ __device__ constexpr int tile_rowb() { return D * 2 + 16; }   // padded row stride (bytes)
+
+inline size_t tile_smem_bytes(int D, int b) {
+  return (size_t)b * (D * 2 + 16) + (size_t)b * (sizeof(float) * 2 + sizeof(unsigned long long));
+}
+
+template <int D>
+__global__ void __launch_bounds__(kTileThreads) k_red_tile(Call c) {
+  if (*c.status != ZPC_OK) return;
+  constexpr int ROWB = tile_rowb<D>();
+  constexpr int CPR = D / 8;                        // 16-B chunks per row
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int b = c.b;
+  uint8_t* st = smem;
+  unsigned long long* last = reinterpret_cast<unsigned long long*>(smem + (size_t)b * ROWB);
+  float* inv_norm = reinterpret_cast<float*>(last + b);
+  float* rowsum = inv_norm + b;
+  const int unit = blockIdx.x;
+  const int h = unit % c.h_kv;
+  const int l = (unit / c.h_kv) % c.L;
+  const int r = unit / (c.h_kv * c.L);
+  const int T = c.seq_lens[r];
+  const int jb = blockIdx.y;
+  if (jb * b >= T) return;
+  const int j0 = jb * b;
+  const int nvalid = min(b, T - j0);
+  const int blk = c.tables[(size_t)r * c.table_stride + jb];
+  const uint16_t* K = reinterpret_cast<const uint16_t*>(c.k_cache);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  // stage the block's rows by 16-B cp.async (16 threads per 256-B row, every copy in flight at once);
+  // slots >= T are zero-filled (src-size 0, R20)
+  const uint32_t st_s = (uint32_t)__cvta_generic_to_shared(st);
+  for (int q = tid; q < b * CPR; q += kTileThreads) {
+    const int row = q / CPR, ch = q % CPR;
+    const bool ok = row < nvalid;
+    const uint16_t* src = K + kv_row(c, l, blk, ok ? row : 0, h) + ch * 8;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(st_s + (uint32_t)(row * ROWB + ch * 16)),
+                 "l"(src), "r"(ok ? 16 : 0)
+                 : "memory");
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  for (int j = tid; j < b; j += kTileThreads) last[j] = 0ull;
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncthreads();
+  // 1/||k_i|| in fp32 (0 for a zero-norm key or an empty slot, R23)
+  for (int i = tid; i < b; i += kTileThreads) {
+    float s = 0.f;
+#pragma unroll
+    for (int ch = 0; ch < CPR; ++ch) {
+      const uint4 v = *reinterpret_cast<const uint4*>(st + i * ROWB + ch * 16);
+      const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float lo = __uint_as_float(w4[e] << 16), hi = __uint_as_float(w4[e] & 0xffff0000u);
+        s = fmaf(lo, lo, s);
+        s = fmaf(hi, hi, s);
+      }
+    }
+    inv_norm[i] = s > 0.f ? 1.0f / sqrtf(s) : 0.f;
+  }
+  __syncthreads();
+
+  const float p = c.red_p;
+  const uint32_t frag_off = (uint32_t)((lane & 15) * ROWB + (lane >> 4) * 16);
+  const int cq = lane & 3;
+  // each warp owns a pair of 16-row stripes (32 rows): every B fragment loaded by ldmatrix feeds
+  // four MMAs, and both stripes' A fragments stay in registers across the column chunks
+  for (int pw = warp; pw * 32 < b; pw += kTileThreads / 32) {
+    const bool two = pw * 32 + 16 < b;               // warp-uniform: the second stripe exists
+    int rr[2][2];
+    float nn[2][2], rs[2][2];
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+      rr[m][0] = pw * 32 + m * 16 + (lane >> 2);
+      rr[m][1] = rr[m][0] + 8;
+      const bool ok = m == 0 || two;
+      nn[m][0] = ok ? inv_norm[rr[m][0]] : 0.f;
+      nn[m][1] = ok ? inv_norm[rr[m][1]] : 0.f;
+      rs[m][0] = rs[m][1] = 0.f;
+    }
+    uint32_t a[2][D / 16][4];
+#pragma unroll
+    for (int m = 0; m < 2; ++m)
+#pragma unroll
+      for (int s = 0; s < D / 16; ++s) {
+        if (m == 1 && !two) { a[m][s][0] = a[m][s][1] = a[m][s][2] = a[m][s][3] = 0u; continue; }
+        ldsm_x4(st_s + (uint32_t)((pw * 32 + m * 16) * ROWB) + frag_off + s * 32, a[m][s][0], a[m][s][1],
+                a[m][s][2], a[m][s][3]);
+      }
+    for (int nc = 0; nc < b; nc += 32) {
+      const bool full = nc + 16 < b;                 // warp-uniform: the chunk's second 16 columns exist
+      float acc[2][4][4];
+#pragma unroll
+      for (int m = 0; m < 2; ++m)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[m][q][0] = acc[m][q][1] = acc[m][q][2] = acc[m][q][3] = 0.f;
+#pragma unroll
+      for (int s = 0; s < D / 16; ++s) {
+#pragma unroll
+        for (int pq = 0; pq < 2; ++pq) {
+          if (pq == 1 && !full) continue;
+          uint32_t x0, x1, x2, x3;
+          ldsm_x4(st_s + (uint32_t)((nc + pq * 16) * ROWB) + frag_off + s * 32, x0, x1, x2, x3);
+#pragma unroll
+          for (int m = 0; m < 2; ++m) {
+            if (m == 1 && !two) continue;
+            mma_bf16(acc[m][2 * pq], a[m][s][0], a[m][s][1], a[m][s][2], a[m][s][3], x0, x2);      // +0..7
+            mma_bf16(acc[m][2 * pq + 1], a[m][s][0], a[m][s][1], a[m][s][2], a[m][s][3], x1, x3);  // +8..15
+          }
+        }
+      }
+#pragma unroll
+      for (int m = 0; m < 2; ++m) {
+        if (m == 1 && !two) continue;
+        const int r1 = rr[m][0], r2 = rr[m][1];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (q >= 2 && !full) break;
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int j = nc + q * 8 + 2 * cq + e;
+            const float nj = inv_norm[j];
+            const float v1 = (j == r1) ? 0.f : acc[m][q][e] * nn[m][0] * nj;
+            const float v2 = (j == r2) ? 0.f : acc[m][q][2 + e] * nn[m][1] * nj;
+            rs[m][0] += v1;
+            rs[m][1] += v2;
+            // this stripe's last row above p in column j; rows of the column sit on the 8 lanes
+            // sharing lane & 3 (skipped, warp-uniformly, when no lane holds a cosine above p)
+            if (!__any_sync(0xffffffffu, v1 > p || v2 > p)) continue;
+            unsigned long long key = v2 > p   ? ((unsigned long long)(r2 + 1) << 32) | __float_as_uint(v2)
+                                     : v1 > p ? ((unsigned long long)(r1 + 1) << 32) | __float_as_uint(v1)
+                                              : 0ull;
+#pragma unroll
+            for (int o = 4; o < 32; o <<= 1) {
+              const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
+              key = other > key ? other : key;
+            }
+            if (lane < 4 && key) atomicMax(&last[j], key);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+      if (m == 1 && !two) continue;
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        float v = rs[m][k];
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        v += __shfl_xor_sync(0xffffffffu, v, 2);
+        if (cq == 0) rowsum[rr[m][k]] = v;
+      }
+    }
+  }
+  __syncthreads();
+  // remove each column's zeroed entry from its row, in ascending column order; r[t] = sum / T
+  float* out = c.ws.redund + (size_t)unit * c.max_seq_len;
+  const float inv_T = 1.0f / (float)T;
+  for (int i0 = warp * 32; i0 < b; i0 += kTileThreads) {
+    const int i = i0 + lane;                         // b is a multiple of 16: i < b for lanes < 16
+    float s = i < b ? rowsum[i] : 0.f;
+    for (int jc = 0; jc < b; jc += 32) {             // columns with a zeroed entry, ascending
+      const unsigned long long key = jc + lane < b ? last[jc + lane] : 0ull;
+      uint32_t any = __ballot_sync(0xffffffffu, key != 0ull);
+      while (any) {
+        const int src = __ffs(any) - 1;
+        any &= any - 1;
+        const unsigned long long k = __shfl_sync(0xffffffffu, key, src);
+        if ((int)(k >> 32) == i + 1) s -= __uint_as_float((uint32_t)k);
+      }
+    }
+    if (i < nvalid) out[j0 + i] = s * inv_T;
+  }
+}
+
 }  // namespace
 
 cudaError_t launch_redundancy(const Call& c, cudaStream_t s) {
@@ -194,6 +382,24 @@ cudaError_t launch_redundancy(const Call& c, cudaStream_t s) {
     const dim3 grid(units, (nb_max + kWarps * kBlocksPerWarp - 1) / (kWarps * kBlocksPerWarp));
     if (c.d == 128) k_red_mma<128><<<grid, kWarps * 32, 0, s>>>(c);
     else k_red_mma<64><<<grid, kWarps * 32, 0, s>>>(c);
+  } else if (c.dtype == ZPC_BF16 && c.b > 16 && c.b % 16 == 0 && c.b <= 256) {
+    const dim3 grid(units, (c.max_seq_len + c.b - 1) / c.b);
+    const size_t smem = tile_smem_bytes(c.d, c.b);
+    cudaError_t e;
+    if (c.d == 128) {
+      e = cudaFuncSetAttribute(k_red_tile<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      // 3 CTAs of b = 256 per SM need the whole carveout
+      e = cudaFuncSetAttribute(k_red_tile<128>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      if (e != cudaSuccess) return e;
+      k_red_tile<128><<<grid, kTileThreads, smem, s>>>(c);
+    } else {
+      e = cudaFuncSetAttribute(k_red_tile<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      e = cudaFuncSetAttribute(k_red_tile<64>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      if (e != cudaSuccess) return e;
+      k_red_tile<64><<<grid, kTileThreads, smem, s>>>(c);
+    }
   } else {
     const int nb_max = (c.max_seq_len + c.b - 1) / c.b;
     const dim3 grid(units, min(64, (nb_max + kWarps - 1) / kWarps));

@@ -29,7 +29,8 @@ bool desc_ok(const zpc_cache_desc* d, const zpc_params* p) {
     if (!std::isfinite(p->redundancy_lambda) || !std::isfinite(p->redundancy_tau) || !std::isfinite(p->redundancy_p)) return false;
     if (p->redundancy_lambda < 0.f || p->redundancy_tau <= 0.f) return false;
     if (p->redundancy_p < 0.f || p->redundancy_p > 1.f) return false;
-    if (d->block_size > 32) return false;   // one warp per block
+    // b <= 32: one warp per block; bf16 b = 48..256 (multiples of 16): the tile kernel
+    if (d->block_size > 32 && !(d->dtype == ZPC_BF16 && d->block_size % 16 == 0 && d->block_size <= 256)) return false;
   }
   if (p->flags & ZPC_F_GLOBAL_SCORE) {
     if (!std::isfinite(p->global_alpha) || p->global_alpha < 0.f || p->global_alpha > 1.f) return false;

@@ -61,7 +61,10 @@ def test_redundancy_region_and_params():
         # without the flag the same values are ignored
         pn = zipc.make_params(129, 7, 8192, 0, **bad)
         assert zipc.zpc_workspace_bytes(_desc(), pn, 4) > 0, bad
-    assert zipc.zpc_workspace_bytes(_desc(b=64), p1, 4) == 0   # one warp per block: b <= 32
+    assert zipc.zpc_workspace_bytes(_desc(b=64, dtype="fp32"), p1, 4) == 0   # fp32: one warp per block, b <= 32
+    assert zipc.zpc_workspace_bytes(_desc(b=40), p1, 4) == 0                   # bf16 tile kernel: multiples of 16
+    assert zipc.zpc_workspace_bytes(_desc(b=512), p1, 4) == 0                  # ... up to 256
+    assert zipc.zpc_workspace_bytes(_desc(b=256), p1, 4) > 0                   # the paper's b = 256
 
 
 @pytest.mark.parametrize("bad", [dict(h_q=30), dict(d=96), dict(w=0), dict(dtype=7), dict(h_q=4 * 9, w=32)])

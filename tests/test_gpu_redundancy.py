@@ -77,6 +77,13 @@ CASES = {
                                wave=0),
     "bf16_b8_generic": scaled(CONFIGS["qwen7b"], L=1, h_kv=2, h_q=14, b=8, n_max=17, seq_lens=[300, 211], budget=128,
                               free_slack=5),
+    # k_red_tile: b = 64 with a ragged last block, and the paper's operating point b = 256
+    "bf16_b64_tile": scaled(CONFIGS["qwen7b"], L=1, h_kv=2, h_q=14, b=64, n_max=5, seq_lens=[300, 270], budget=200,
+                            free_slack=5),
+    "bf16_b256_tile": scaled(CONFIGS["paper_op"], L=2, h_kv=2, h_q=8, seq_lens=[2304, 2149], budget=2048, wave=0,
+                             free_slack=4),
+    "bf16_b48_d64_tile": scaled(CONFIGS["qwen32b"], L=1, h_kv=2, h_q=10, d=64, b=48, n_max=6, seq_lens=[250, 290],
+                                budget=200, wave=0, free_slack=4),
 }
 
 
@@ -102,7 +109,9 @@ def test_redundancy_rows_match_oracle(cuda_ok, name):
 
 
 @pytest.mark.parametrize("name,stages", [("fp32_toy_b4_generic", False), ("bf16_7b_b16_mma", False),
-                                         ("bf16_7b_b16_mma", True), ("bf16_32b_d64_mma", False)])
+                                         ("bf16_7b_b16_mma", True), ("bf16_32b_d64_mma", False),
+                                         ("bf16_b64_tile", False), ("bf16_b256_tile", False),
+                                         ("bf16_b256_tile", True), ("bf16_b48_d64_tile", False)])
 def test_redundancy_compress_parity(cuda_ok, name, stages):
     cfg = CASES[name]
     w, inp, res = _run(cfg, seed=22, stages=stages)
