@@ -199,7 +199,8 @@ template <int D>
 __host__ __device__ constexpr int tile_rowb() { return D * 2 + 16; }   // padded row stride (bytes)
 
 inline size_t tile_smem_bytes(int D, int b) {
-  return (size_t)b * (D * 2 + 16) + (size_t)b * (sizeof(float) * 2 + sizeof(unsigned long long));
+  return (size_t)b * (D * 2 + 16) + (size_t)b * (sizeof(float) * 2 + sizeof(unsigned long long)) +
+         (size_t)(b / 16) * b * sizeof(float);
 }
 
 template <int D>
@@ -213,6 +214,7 @@ __global__ void __launch_bounds__(kTileThreads) k_red_tile(Call c) {
   unsigned long long* last = reinterpret_cast<unsigned long long*>(smem + (size_t)b * ROWB);
   float* inv_norm = reinterpret_cast<float*>(last + b);
   float* rowsum = inv_norm + b;
+  float* colpart = rowsum + b;                       // [b/16][b] column sums of mirrored tiles
   const int unit = blockIdx.x;
   const int h = unit % c.h_kv;
   const int l = (unit / c.h_kv) % c.L;
@@ -262,79 +264,116 @@ __global__ void __launch_bounds__(kTileThreads) k_red_tile(Call c) {
   const float p = c.red_p;
   const uint32_t frag_off = (uint32_t)((lane & 15) * ROWB + (lane >> 4) * 16);
   const int cq = lane & 3;
-  // each warp owns a pair of 16-row stripes (32 rows): every B fragment loaded by ldmatrix feeds
-  // four MMAs, and both stripes' A fragments stay in registers across the column chunks
-  for (int pw = warp; pw * 32 < b; pw += kTileThreads / 32) {
-    const bool two = pw * 32 + 16 < b;               // warp-uniform: the second stripe exists
+  // C is symmetric: only the tiles (stripe m, column group n >= m) of 16 x 16 are formed. Warp w owns
+  // stripes w and MT-1-w (MT + 1 tiles per warp for even MT): for n >= MT-1-w one ldmatrix B fragment
+  // feeds both stripes' MMAs. An off-diagonal tile (n > m) also stands for its mirror (n, m): its
+  // column sums go to colpart[m][j] (summed in ascending m at the end, deterministic) and each row's
+  // last column above p is a candidate for the column i = that row.
+  const int MT = b / 16;
+  for (int w2 = warp; 2 * w2 < MT; w2 += kTileThreads / 32) {
+    const int ms[2] = {w2, MT - 1 - w2};
+    const bool two = ms[1] != ms[0];                 // warp-uniform: a distinct second stripe
     int rr[2][2];
     float nn[2][2], rs[2][2];
 #pragma unroll
     for (int m = 0; m < 2; ++m) {
-      rr[m][0] = pw * 32 + m * 16 + (lane >> 2);
+      rr[m][0] = ms[m] * 16 + (lane >> 2);
       rr[m][1] = rr[m][0] + 8;
-      const bool ok = m == 0 || two;
-      nn[m][0] = ok ? inv_norm[rr[m][0]] : 0.f;
-      nn[m][1] = ok ? inv_norm[rr[m][1]] : 0.f;
+      nn[m][0] = inv_norm[rr[m][0]];
+      nn[m][1] = inv_norm[rr[m][1]];
       rs[m][0] = rs[m][1] = 0.f;
     }
     uint32_t a[2][D / 16][4];
 #pragma unroll
     for (int m = 0; m < 2; ++m)
 #pragma unroll
-      for (int s = 0; s < D / 16; ++s) {
-        if (m == 1 && !two) { a[m][s][0] = a[m][s][1] = a[m][s][2] = a[m][s][3] = 0u; continue; }
-        ldsm_x4(st_s + (uint32_t)((pw * 32 + m * 16) * ROWB) + frag_off + s * 32, a[m][s][0], a[m][s][1],
-                a[m][s][2], a[m][s][3]);
-      }
-    for (int nc = 0; nc < b; nc += 32) {
-      const bool full = nc + 16 < b;                 // warp-uniform: the chunk's second 16 columns exist
-      float acc[2][4][4];
+      for (int s = 0; s < D / 16; ++s)
+        ldsm_x4(st_s + (uint32_t)(ms[m] * 16 * ROWB) + frag_off + s * 32, a[m][s][0], a[m][s][1], a[m][s][2],
+                a[m][s][3]);
+    for (int n = ms[0]; n < MT; ++n) {               // column group n: columns 16n .. 16n+15
+      const bool useB = two && n >= ms[1];
+      float acc[2][2][4];
 #pragma unroll
       for (int m = 0; m < 2; ++m)
 #pragma unroll
-        for (int q = 0; q < 4; ++q) acc[m][q][0] = acc[m][q][1] = acc[m][q][2] = acc[m][q][3] = 0.f;
+        for (int q = 0; q < 2; ++q) acc[m][q][0] = acc[m][q][1] = acc[m][q][2] = acc[m][q][3] = 0.f;
 #pragma unroll
       for (int s = 0; s < D / 16; ++s) {
-#pragma unroll
-        for (int pq = 0; pq < 2; ++pq) {
-          if (pq == 1 && !full) continue;
-          uint32_t x0, x1, x2, x3;
-          ldsm_x4(st_s + (uint32_t)((nc + pq * 16) * ROWB) + frag_off + s * 32, x0, x1, x2, x3);
-#pragma unroll
-          for (int m = 0; m < 2; ++m) {
-            if (m == 1 && !two) continue;
-            mma_bf16(acc[m][2 * pq], a[m][s][0], a[m][s][1], a[m][s][2], a[m][s][3], x0, x2);      // +0..7
-            mma_bf16(acc[m][2 * pq + 1], a[m][s][0], a[m][s][1], a[m][s][2], a[m][s][3], x1, x3);  // +8..15
-          }
+        uint32_t x0, x1, x2, x3;
+        ldsm_x4(st_s + (uint32_t)(n * 16 * ROWB) + frag_off + s * 32, x0, x1, x2, x3);
+        mma_bf16(acc[0][0], a[0][s][0], a[0][s][1], a[0][s][2], a[0][s][3], x0, x2);      // +0..7
+        mma_bf16(acc[0][1], a[0][s][0], a[0][s][1], a[0][s][2], a[0][s][3], x1, x3);      // +8..15
+        if (useB) {
+          mma_bf16(acc[1][0], a[1][s][0], a[1][s][1], a[1][s][2], a[1][s][3], x0, x2);
+          mma_bf16(acc[1][1], a[1][s][0], a[1][s][1], a[1][s][2], a[1][s][3], x1, x3);
         }
       }
 #pragma unroll
       for (int m = 0; m < 2; ++m) {
-        if (m == 1 && !two) continue;
+        if (m == 1 && !useB) continue;
         const int r1 = rr[m][0], r2 = rr[m][1];
+        const bool mirror = n > ms[m];               // warp-uniform
+        // this lane's 4 columns jc(k) = 16n + (k >> 1) * 8 + 2 * (lane & 3) + (k & 1), rows r1 and r2
+        float v1[4], v2[4];
+        bool hit = false;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          if (q >= 2 && !full) break;
+        for (int k = 0; k < 4; ++k) {
+          const int j = n * 16 + (k >> 1) * 8 + 2 * cq + (k & 1);
+          const float nj = inv_norm[j];
+          v1[k] = (j == r1) ? 0.f : acc[m][k >> 1][k & 1] * nn[m][0] * nj;
+          v2[k] = (j == r2) ? 0.f : acc[m][k >> 1][2 + (k & 1)] * nn[m][1] * nj;
+          rs[m][0] += v1[k];
+          rs[m][1] += v2[k];
+          hit |= (v1[k] > p) | (v2[k] > p);
+        }
+        if (mirror) {
+          // C[j][i] summed over the stripe's 16 rows i: the lane's 4 column partials reduced over the 8
+          // lanes sharing lane & 3 by a halving butterfly (bits 4, 3, then 2 of the lane: 4 shuffles)
+          float cs[4];
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int j = nc + q * 8 + 2 * cq + e;
-            const float nj = inv_norm[j];
-            const float v1 = (j == r1) ? 0.f : acc[m][q][e] * nn[m][0] * nj;
-            const float v2 = (j == r2) ? 0.f : acc[m][q][2 + e] * nn[m][1] * nj;
-            rs[m][0] += v1;
-            rs[m][1] += v2;
-            // this stripe's last row above p in column j; rows of the column sit on the 8 lanes
-            // sharing lane & 3 (skipped, warp-uniformly, when no lane holds a cosine above p)
-            if (!__any_sync(0xffffffffu, v1 > p || v2 > p)) continue;
-            unsigned long long key = v2 > p   ? ((unsigned long long)(r2 + 1) << 32) | __float_as_uint(v2)
-                                     : v1 > p ? ((unsigned long long)(r1 + 1) << 32) | __float_as_uint(v1)
-                                              : 0ull;
+          for (int k = 0; k < 4; ++k) cs[k] = v1[k] + v2[k];
+          const bool h16 = lane & 16, h8 = lane & 8;
+          const float k0 = (h16 ? cs[2] : cs[0]) + __shfl_xor_sync(0xffffffffu, h16 ? cs[0] : cs[2], 16);
+          const float k1 = (h16 ? cs[3] : cs[1]) + __shfl_xor_sync(0xffffffffu, h16 ? cs[1] : cs[3], 16);
+          float t = (h8 ? k1 : k0) + __shfl_xor_sync(0xffffffffu, h8 ? k0 : k1, 8);
+          t += __shfl_xor_sync(0xffffffffu, t, 4);
+          const int kk = (h16 ? 2 : 0) + (h8 ? 1 : 0);
+          if (!(lane & 4)) colpart[ms[m] * b + n * 16 + (kk >> 1) * 8 + 2 * cq + (kk & 1)] = t;
+        }
+        // rare path (warp-uniform): some cosine of this tile is above p
+        if (__any_sync(0xffffffffu, hit)) {
+          unsigned long long kr1 = 0ull, kr2 = 0ull;  // rows' last column above p (mirror candidates)
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int j = n * 16 + (k >> 1) * 8 + 2 * cq + (k & 1);
+            if (mirror) {                            // columns ascend with k: the last one above p wins
+              if (v1[k] > p) kr1 = ((unsigned long long)(j + 1) << 32) | __float_as_uint(v1[k]);
+              if (v2[k] > p) kr2 = ((unsigned long long)(j + 1) << 32) | __float_as_uint(v2[k]);
+            }
+            // the stripe's last row above p in column j; the column's rows sit on the 8 lanes sharing
+            // lane & 3
+            unsigned long long key = v2[k] > p   ? ((unsigned long long)(r2 + 1) << 32) | __float_as_uint(v2[k])
+                                     : v1[k] > p ? ((unsigned long long)(r1 + 1) << 32) | __float_as_uint(v1[k])
+                                                 : 0ull;
 #pragma unroll
             for (int o = 4; o < 32; o <<= 1) {
               const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
               key = other > key ? other : key;
             }
             if (lane < 4 && key) atomicMax(&last[j], key);
+          }
+          // mirror: column r's candidates are the rows j (> r) of group n, i.e. row r's columns, which
+          // sit on the 4 lanes sharing lane >> 2
+          if (mirror) {
+#pragma unroll
+            for (int o = 1; o < 4; o <<= 1) {
+              const unsigned long long o1 = __shfl_xor_sync(0xffffffffu, kr1, o);
+              const unsigned long long o2 = __shfl_xor_sync(0xffffffffu, kr2, o);
+              kr1 = o1 > kr1 ? o1 : kr1;
+              kr2 = o2 > kr2 ? o2 : kr2;
+            }
+            if (cq == 0 && kr1) atomicMax(&last[r1], kr1);
+            if (cq == 0 && kr2) atomicMax(&last[r2], kr2);
           }
         }
       }
@@ -357,7 +396,11 @@ __global__ void __launch_bounds__(kTileThreads) k_red_tile(Call c) {
   const float inv_T = 1.0f / (float)T;
   for (int i0 = warp * 32; i0 < b; i0 += kTileThreads) {
     const int i = i0 + lane;                         // b is a multiple of 16: i < b for lanes < 16
-    float s = i < b ? rowsum[i] : 0.f;
+    float s = 0.f;
+    if (i < b) {                                     // own-stripe tiles + mirrored tiles of stripes above
+      s = rowsum[i];
+      for (int m = 0; m < i / 16; ++m) s += colpart[m * b + i];
+    }
     for (int jc = 0; jc < b; jc += 32) {             // columns with a zeroed entry, ascending
       const unsigned long long key = jc + lane < b ? last[jc + lane] : 0ull;
       uint32_t any = __ballot_sync(0xffffffffu, key != 0ull);

@@ -37,11 +37,11 @@ LAM, TAU, P = 0.2, 0.4, 0.8
 MARGIN = 2e-5
 
 
-def _run(cfg, seed, stages=False):
+def _run(cfg, seed, stages=False, p=P):
     hw = make_host_workload(cfg, seed)
     w = from_host(hw)
     inp = snapshot_inputs(w)
-    desc, params = desc_params(w, redundancy=(LAM, TAU, P))
+    desc, params = desc_params(w, redundancy=(LAM, TAU, p))
     b = batch_of(w, desc, params)
     if stages:
         for fn in (zipc.zpc_plan, zipc.zpc_score, zipc.zpc_redundancy, zipc.zpc_select, zipc.zpc_compact,
@@ -106,6 +106,36 @@ def test_redundancy_rows_match_oracle(cuda_ok, name):
                 np.testing.assert_allclose(got, ref, rtol=1e-5, atol=4e-5 / T, err_msg=f"{name} r={r} l={l} h={h}")
                 checked += 1
     assert checked >= max(1, (len(inp["seq"]) * cfg.L * cfg.h_kv) // 2), f"too many ambiguous units ({checked})"
+
+
+P_LOW = 0.35   # ~4 standard deviations of a random 128-d cosine: a few dozen pairs per unit lie above it
+
+
+@pytest.mark.parametrize("name", [n for n in CASES if "toy" not in n])
+def test_redundancy_rows_zeroing_exercised(cuda_ok, name):
+    """At p = 0.8 random keys never reach the threshold, so the "last row above p" zeroing
+    would go untested; at p = 0.35 several cosines per unit exceed it (asserted), through every kernel."""
+    cfg = CASES[name]
+    w, inp, res = _run(cfg, seed=24, p=P_LOW)
+    geo = geometry(w)
+    kf = O.widen(inp["k"], cfg.dtype)
+    checked = above = 0
+    for r in range(len(inp["seq"])):
+        T = int(inp["seq"][r])
+        for l in range(cfg.L):
+            for h in range(cfg.h_kv):
+                keys = O.unit_keys(geo, kf, inp["tables"][r], T, l, h)
+                if _min_margin(keys, cfg.b, P_LOW) < MARGIN:
+                    continue
+                for j0 in range(0, T, cfg.b):
+                    C = O.cosine_matrix(keys[j0:j0 + cfg.b])
+                    above += int((C[~np.eye(C.shape[0], dtype=bool)] > P_LOW).sum())
+                ref = O.lightning_redundancy_raw(keys, cfg.b, P_LOW)
+                got = res["r"][unit_index(w, r, l, h), :T]
+                np.testing.assert_allclose(got, ref, rtol=1e-5, atol=4e-5 / T, err_msg=f"{name} r={r} l={l} h={h}")
+                checked += 1
+    assert checked >= max(1, (len(inp["seq"]) * cfg.L * cfg.h_kv) // 2), f"too many ambiguous units ({checked})"
+    assert above > 0, "no cosine above p: the zeroing rule was not exercised"
 
 
 @pytest.mark.parametrize("name,stages", [("fp32_toy_b4_generic", False), ("bf16_7b_b16_mma", False),
