@@ -39,7 +39,16 @@ constexpr int kEpiWarp0 = 8;     // first epilogue warp (warps 8..15: lane quart
 #ifndef ZPC_POLY
 #define ZPC_POLY 0
 #endif
-constexpr bool kPolyOffload = ZPC_POLY != 0;   // 25% of pass-1 exp2 on the FMA pipe (pays off only when MUFU-bound)
+// ZPC_POLY = k: k of every 8 pass-1 exp2 pairs on the FMA pipe (ex2_poly2) instead of MUFU.
+// ZPC_POLY_SPLIT: the same for k_score_ovl's token-split instances (G*w <= 128), where the two warps
+// of a lane quarter both run the pass-1 exp chain and the MUFU is the busiest pipe. Measured on one
+// B200 (gpurun_out A/B, score ms): llama8b (G*w = 128) 13.13 / 12.36 / 12.46 / 13.02 / 13.40 for
+// k = 0 / 1 / 2 / 3 / 4; qwen7b (G*w = 224) 8.07 / 8.17 / 8.46 / 8.71 / 9.03 -> defaults 0 and 1.
+#ifndef ZPC_POLY_SPLIT
+#define ZPC_POLY_SPLIT 1
+#endif
+constexpr int kPolyEighths = ZPC_POLY;
+__host__ __device__ constexpr bool poly_pair(int j, int pe = kPolyEighths) { return pe != 0 && (j & 7) >= 8 - pe; }
 constexpr int kIdSlots = 8;      // block-id ring of the feeder warp (tiles in flight + 2 being read)
 constexpr int kIdAhead = 4;      // tiles whose ids the feeder has in flight ahead of the published one
 constexpr int kMaxIds = 32;      // block ids per 128-token tile (b >= 5)
@@ -372,10 +381,10 @@ struct Cfg {
   static_assert(Q_BYTES % 1024 == 0, "Q slabs must stay 1024-B aligned for SW128");
 };
 
-// 2^x on MUFU for most pairs, on the FMA pipe for pairs j % 4 == 3 (25%): balances the two pipes.
+// 2^x on MUFU for most pairs, on the FMA pipe for ZPC_POLY of every 8 pairs: balances the two pipes.
 template <int J>
 __device__ __forceinline__ uint64_t ex2_pair(uint64_t a2) {
-  if constexpr (kPolyOffload && (J & 3) == 3) {
+  if constexpr (poly_pair(J, kPolyEighths)) {
     return ex2_poly2(a2);
   } else {
     float a0, a1;
@@ -393,14 +402,14 @@ __device__ __forceinline__ void sum_exp_rec(const float* v, uint64_t S2, uint64_
     sum_exp_rec<J + 1>(v, S2, NM2, acc);
   }
 }
-template <int N>
+template <int N, int PE = kPolyEighths>
 __device__ __forceinline__ float sum_exp_n(const float* v, float scale, float m) {
   uint64_t acc[4] = {0, 0, 0, 0};
   const uint64_t S2 = pk2(scale, scale), NM2 = pk2(-m, -m);
 #pragma unroll
   for (int j = 0; j < N / 2; ++j) {
     const uint64_t arg = fma2(pk2(v[2 * j], v[2 * j + 1]), S2, NM2);
-    if (kPolyOffload && (j & 3) == 3) {
+    if (poly_pair(j, PE)) {
       acc[j & 3] = add2(acc[j & 3], ex2_poly2(arg));
     } else {
       float a0, a1;
@@ -1404,7 +1413,7 @@ __global__ void __launch_bounds__(kThreadsO, 1) k_score_ovl(Call c, const __grid
           const float mn = fmaxf(mm, mx * scale);
           const float mref = mn > -INFINITY ? mn : 0.f;
           const float rescale = ex2f(mm - mref);
-          const float bsum = sum_exp_n<NB>(v, scale, mref);
+          const float bsum = sum_exp_n<NB, kSplit ? ZPC_POLY_SPLIT : kPolyEighths>(v, scale, mref);
           ss = ss * rescale + bsum;
           mm = mn;
         };
