@@ -47,6 +47,9 @@ constexpr int kEpiWarp0 = 8;     // first epilogue warp (warps 8..15: lane quart
 #ifndef ZPC_POLY_SPLIT
 #define ZPC_POLY_SPLIT 1
 #endif
+#ifndef ZPC_POLY_TC   // k_score_tc's pass 1 (the w = 16 calls of the paper's operating point)
+#define ZPC_POLY_TC ZPC_POLY
+#endif
 constexpr int kPolyEighths = ZPC_POLY;
 __host__ __device__ constexpr bool poly_pair(int j, int pe = kPolyEighths) { return pe != 0 && (j & 7) >= 8 - pe; }
 constexpr int kIdSlots = 8;      // block-id ring of the feeder warp (tiles in flight + 2 being read)
@@ -884,7 +887,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
             const float mn = fmaxf(mm, mx * scale);             // -inf only if nothing valid yet
             const float mref = mn > -INFINITY ? mn : 0.f;
             const float rescale = ex2f(mm - mref);              // mm = -inf -> 0 (ss is 0 anyway)
-            const float bsum = sum_exp_n<NB>(v, scale, mref);
+            const float bsum = sum_exp_n<NB, ZPC_POLY_TC>(v, scale, mref);
             ss = ss * rescale + bsum;
             mm = mn;
           };
