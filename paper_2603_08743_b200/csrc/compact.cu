@@ -10,14 +10,13 @@
 // Rows move as 16-byte vectors, coalesced along d; a chunk is kVec vectors per tensor per thread
 // (VPR = vectors per row is a template parameter). HBM-bound: the bytes in flight per SM decide
 // the rate, and many small CTAs (16 per SM) beat deep per-thread buffering (launch_compact).
+#include <cstdlib>
+
 #include "internal.h"
 
 namespace zpc {
 namespace {
 
-constexpr int kThreads = 128;
-constexpr int kVecPerThread = 1;   // 16-B vectors per tensor per thread per chunk
-constexpr int kMinCtas = 16;       // resident CTAs per SM (2048 threads)
 
 template <int VPR, int kVec>
 struct Chunk {
@@ -27,7 +26,7 @@ struct Chunk {
   uint32_t fdst[kVec];               // its destination row (blk*b + slot), ~0u = none
 };
 
-template <int VPR, int kVec>
+template <int VPR, int kVec, int kThreads>
 __device__ __forceinline__ void load_chunk(const Call& c, Chunk<VPR, kVec>& ch, int base, int ell, const int32_t* kept,
                                            const int32_t* table, const int32_t* tg, const int4* K, const int4* V,
                                            size_t plane, int bsh, const float* F, size_t fplane) {
@@ -66,7 +65,7 @@ __device__ __forceinline__ void load_chunk(const Call& c, Chunk<VPR, kVec>& ch, 
   }
 }
 
-template <int VPR, int kVec, int kMinCtas>
+template <int VPR, int kVec, int kThreads, int kMinCtas>
 __global__ void __launch_bounds__(kThreads, kMinCtas) k_compact(Call c) {
   if (*c.status != ZPC_OK) return;
   constexpr int CH = kVec * kThreads / VPR;
@@ -91,11 +90,11 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_compact(Call c) {
   unsigned moved = 0;
 
   Chunk<VPR, kVec> cur, nxt;
-  if (ell > 0) load_chunk<VPR, kVec>(c, cur, 0, ell, kept, table, tg, K, V, plane, bsh, Fw, fplane);
+  if (ell > 0) load_chunk<VPR, kVec, kThreads>(c, cur, 0, ell, kept, table, tg, K, V, plane, bsh, Fw, fplane);
   for (int base = 0; base < ell; base += CH) {
     __syncthreads();   // every read of chunk `base` has returned before any write of it
     const bool more = base + CH < ell;
-    if (more) load_chunk<VPR, kVec>(c, nxt, base + CH, ell, kept, table, tg, K, V, plane, bsh, Fw, fplane);
+    if (more) load_chunk<VPR, kVec, kThreads>(c, nxt, base + CH, ell, kept, table, tg, K, V, plane, bsh, Fw, fplane);
 #pragma unroll
     for (int k = 0; k < kVec; ++k) {
       if (cur.dst[k] != ~0u) {
@@ -120,13 +119,33 @@ cudaError_t launch_compact(const Call& c, cudaStream_t s) {
   if (units == 0) return cudaSuccess;
   const int vpr = c.d * (c.dtype == ZPC_BF16 ? 2 : 4) / 16;   // head_dim is 64 or 128 (validated)
   // measured (7B shape, 14.6 M moved rows): thread-level parallelism wins over per-thread depth --
-  // 1 vector/thread at 16 CTAs/SM 2.60 ms (88% of copy peak), 2 @ 8: 2.88, 4 @ 5: 3.21, 8 @ 3: 4.21
+  // 1 vector/thread at 16 CTAs/SM 2.60 ms (88% of copy peak), 2 @ 8: 2.88, 4 @ 5: 3.21, 8 @ 3: 4.21.
+  // With fewer units than 12 CTAs per SM (the paper's operating point: 4 requests x 36 x 8 = 1152 units
+  // for 148 SMs) the threads in flight per SM fall with the CTA count, so those calls run 256-thread CTAs
+  // (8 per SM, the same 32 registers per thread) instead. ZPC_COMPACT_NT = 128 / 256 overrides (A/B runs).
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      sms = 148;
+  }
+  int nt = units >= sms * 12 ? 128 : 256;
+  if (const char* e = getenv("ZPC_COMPACT_NT")) {
+    const int v = atoi(e);
+    if (v == 128 || v == 256) nt = v;
+  }
+#define ZPC_COMPACT_CASE(VPR)                                                      \
+  case VPR:                                                                       \
+    if (nt == 128) k_compact<VPR, 1, 128, 16><<<units, 128, 0, s>>>(c);           \
+    else k_compact<VPR, 1, 256, 8><<<units, 256, 0, s>>>(c);                      \
+    break;
   switch (vpr) {
-    case 8: k_compact<8, kVecPerThread, kMinCtas><<<units, kThreads, 0, s>>>(c); break;
-    case 16: k_compact<16, kVecPerThread, kMinCtas><<<units, kThreads, 0, s>>>(c); break;
-    case 32: k_compact<32, kVecPerThread, kMinCtas><<<units, kThreads, 0, s>>>(c); break;
+    ZPC_COMPACT_CASE(8)
+    ZPC_COMPACT_CASE(16)
+    ZPC_COMPACT_CASE(32)
     default: return cudaErrorInvalidValue;
   }
+#undef ZPC_COMPACT_CASE
   return cudaGetLastError();
 }
 
