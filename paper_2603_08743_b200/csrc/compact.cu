@@ -9,7 +9,8 @@
 // are issued before the stores of chunk j (software pipelining).
 // Rows move as 16-byte vectors, coalesced along d; a chunk is kVec vectors per tensor per thread
 // (VPR = vectors per row is a template parameter). HBM-bound: the bytes in flight per SM decide
-// the rate, and many small CTAs (16 per SM) beat deep per-thread buffering (launch_compact).
+// the rate: one vector per thread, CTA width chosen per call so ~2048 threads per SM are in flight
+// (launch_compact).
 #include <cstdlib>
 
 #include "internal.h"
@@ -118,26 +119,31 @@ cudaError_t launch_compact(const Call& c, cudaStream_t s) {
   const int units = c.R * c.L * c.h_kv;
   if (units == 0) return cudaSuccess;
   const int vpr = c.d * (c.dtype == ZPC_BF16 ? 2 : 4) / 16;   // head_dim is 64 or 128 (validated)
-  // measured (7B shape, 14.6 M moved rows): thread-level parallelism wins over per-thread depth --
-  // 1 vector/thread at 16 CTAs/SM 2.60 ms (88% of copy peak), 2 @ 8: 2.88, 4 @ 5: 3.21, 8 @ 3: 4.21.
-  // With fewer units than 12 CTAs per SM (the paper's operating point: 4 requests x 36 x 8 = 1152 units
-  // for 148 SMs) the threads in flight per SM fall with the CTA count, so those calls run 256-thread CTAs
-  // (8 per SM, the same 32 registers per thread) instead. ZPC_COMPACT_NT = 128 / 256 overrides (A/B runs).
+  // One CTA per unit; the CTA width is picked so the threads in flight per SM stay near 2048 (the copy
+  // is latency-bound: bytes in flight per SM decide the rate, and deeper per-thread buffering measured
+  // slower than more threads: 7B shape 1 vector/thread at 16 CTAs/SM 2.60 ms, 2 @ 8: 2.88, 4 @ 5: 3.21).
+  // A/B on one B200 (ZPC_COMPACT_NT, compact ms by CTA width 128 / 256 / 512 / 1024):
+  //   paper_op 1 request  (288 units,  ~2 per SM): 0.336 / 0.201 / 0.143 / 0.117
+  //   paper_op 2 requests (576 units,  ~4 per SM): 0.373 / 0.266 / 0.219 / 0.230
+  //   paper_op 4 requests (1152 units, ~8 per SM): 0.495 / 0.402 / 0.429 / 0.453
+  //   qwen7b 64 requests  (7168 units, 48 per SM): 2.620 / 2.535 / 2.672 / 2.772
   static int sms = 0;
   if (sms == 0) {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
       sms = 148;
   }
-  int nt = units >= sms * 12 ? 128 : 256;
+  int nt = units >= sms * 6 ? 256 : (units >= sms * 3 ? 512 : 1024);
   if (const char* e = getenv("ZPC_COMPACT_NT")) {
     const int v = atoi(e);
-    if (v == 128 || v == 256) nt = v;
+    if (v == 128 || v == 256 || v == 512 || v == 1024) nt = v;
   }
 #define ZPC_COMPACT_CASE(VPR)                                                      \
   case VPR:                                                                       \
     if (nt == 128) k_compact<VPR, 1, 128, 16><<<units, 128, 0, s>>>(c);           \
-    else k_compact<VPR, 1, 256, 8><<<units, 256, 0, s>>>(c);                      \
+    else if (nt == 256) k_compact<VPR, 1, 256, 8><<<units, 256, 0, s>>>(c);       \
+    else if (nt == 512) k_compact<VPR, 1, 512, 4><<<units, 512, 0, s>>>(c);       \
+    else k_compact<VPR, 1, 1024, 2><<<units, 1024, 0, s>>>(c);                    \
     break;
   switch (vpr) {
     ZPC_COMPACT_CASE(8)
