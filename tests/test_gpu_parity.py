@@ -224,3 +224,14 @@ def test_select_reg_other_pools(cuda_ok, monkeypatch, pool):
     cfg = scaled(CONFIGS["qwen7b"], L=1, h_kv=4, h_q=28, n_max=9, seq_lens=[300, 1100, 144, 385],
                  budget=(32, 128), wave=0, free_slack=6, pool_kernel=pool)
     _run(cfg, seed=23, pool=pool, max_seq_len=2048)
+
+
+@pytest.mark.parametrize("nt", [128, 256, 512, 1024])
+def test_compact_every_cta_width(cuda_ok, monkeypatch, nt):
+    """k_compact at each CTA width launch_compact can pick (ZPC_COMPACT_NT overrides the per-call choice):
+    chunk = NT/VPR ranks, so the hazard ordering (reads of a chunk before its writes, kept[i] >= i) is
+    exercised at 8..128 ranks per chunk, for VPR = 16 (bf16 d = 128) and VPR = 8 (bf16 d = 64)."""
+    monkeypatch.setenv("ZPC_COMPACT_NT", str(nt))
+    _run(SMALL7B, seed=40 + nt)
+    cfg = scaled(CONFIGS["qwen32b"], L=2, h_kv=2, h_q=10, d=64, n_max=6, seq_lens=[200, 333], budget=80, wave=0)
+    _run(cfg, seed=41 + nt)
