@@ -23,6 +23,12 @@ struct Ws {
   int32_t* priv_off;       // [R]  exclusive scan of private frees
   int32_t* glob;           // [8]  0: total_fresh 1: total_priv 2: top_base 3: n_zeroed
   int32_t* marks;          // [N_total] shared blocks driven to 0 (ZPC_F_PREFIX)
+  // cooperative score kernel (score_coop.cu): per-chunk partial log2-sum-exp, per-(unit, CTA) arrival
+  // counters, the round plan (first unit of each round + the round count)
+  float* coop_part;        // [units][coop_cmax][G*w]
+  int32_t* coop_cnt;       // [units][2]
+  int32_t* coop_rs;        // [units + 2]
+  int32_t coop_cmax;       // chunks per unit the part array holds
   int32_t kept_stride;
 };
 
@@ -70,6 +76,11 @@ cudaError_t launch_plan(const Call& c, cudaStream_t s);
 cudaError_t launch_finalize(const Call& c, cudaStream_t s);
 cudaError_t launch_score_cudacore(const Call& c, cudaStream_t s);
 cudaError_t launch_score_tc(const Call& c, cudaStream_t s, bool* used);
+cudaError_t launch_score_coop(const Call& c, cudaStream_t s, bool* used);
+// smallest chunk of the cooperative score kernel (pair-tiles of 256 tokens per chunk): sizes the per-unit
+// chunk bound of the workspace partials
+constexpr int kCoopChunkTiles = 4;
+inline int coop_cmax(int max_seq_len) { return ((max_seq_len + 255) / 256 + kCoopChunkTiles - 1) / kCoopChunkTiles; }
 cudaError_t launch_select(const Call& c, cudaStream_t s);
 cudaError_t launch_compact(const Call& c, cudaStream_t s);
 cudaError_t launch_redundancy(const Call& c, cudaStream_t s);

@@ -40,7 +40,8 @@ bool desc_ok(const zpc_cache_desc* d, const zpc_params* p) {
 
 struct LayoutSizes {
   zpc_workspace_layout pub;
-  size_t req_err, n_blocks, fresh_off, priv_off, glob, marks;
+  size_t req_err, n_blocks, fresh_off, priv_off, glob, marks, coop_part, coop_cnt, coop_rs;
+  int32_t coop_cmax;
 };
 
 bool compute_layout(const zpc_cache_desc* d, const zpc_params* p, int32_t R, LayoutSizes* o) {
@@ -66,6 +67,10 @@ bool compute_layout(const zpc_cache_desc* d, const zpc_params* p, int32_t R, Lay
   o->priv_off = take((size_t)R * sizeof(int32_t));
   o->glob = take(8 * sizeof(int32_t));
   o->marks = take((size_t)d->num_blocks * sizeof(int32_t));
+  o->coop_cmax = coop_cmax(p->max_seq_len);
+  o->coop_part = take(units * o->coop_cmax * G * d->window * sizeof(float));
+  o->coop_cnt = take(units * 2 * sizeof(int32_t));
+  o->coop_rs = take((units + 2) * sizeof(int32_t));
   o->pub.total_bytes = off;
   o->pub.kept_stride = kept_stride;
   return true;
@@ -123,6 +128,10 @@ int make_call(const zpc_cache_desc* d, const zpc_params* p, const zpc_batch* b, 
   c->ws.priv_off = reinterpret_cast<int32_t*>(w + ls.priv_off);
   c->ws.glob = reinterpret_cast<int32_t*>(w + ls.glob);
   c->ws.marks = reinterpret_cast<int32_t*>(w + ls.marks);
+  c->ws.coop_part = reinterpret_cast<float*>(w + ls.coop_part);
+  c->ws.coop_cnt = reinterpret_cast<int32_t*>(w + ls.coop_cnt);
+  c->ws.coop_rs = reinterpret_cast<int32_t*>(w + ls.coop_rs);
+  c->ws.coop_cmax = ls.coop_cmax;
   c->ws.kept_stride = ls.pub.kept_stride;
   return ZPC_OK;
 }
@@ -132,7 +141,10 @@ inline int cuda_rc(cudaError_t e) { return e == cudaSuccess ? ZPC_OK : ZPC_ERR_C
 int run_score(const Call& c, cudaStream_t s) {
   if (c.dtype == ZPC_BF16 && !(c.flags & ZPC_F_SCORE_CUDACORE)) {
     bool used = false;
-    cudaError_t e = launch_score_tc(c, s, &used);
+    cudaError_t e = launch_score_coop(c, s, &used);
+    if (e != cudaSuccess) return ZPC_ERR_CUDA;
+    if (used) return ZPC_OK;
+    e = launch_score_tc(c, s, &used);
     if (e != cudaSuccess) return ZPC_ERR_CUDA;
     if (used) return ZPC_OK;
   }
