@@ -50,8 +50,9 @@ constexpr int kCP1Warps = 16;
 constexpr int kCP2Warps = 4;
 constexpr int kCThreads = (kCEpi0 + kCP1Warps + kCP2Warps) * 32;   // 896: 72 registers per thread at launch
 constexpr int kCProdRegs = 48;
-constexpr int kCP2Regs = 112;
-static_assert(8 * kCProdRegs + kCP1Warps * 72 + kCP2Warps * kCP2Regs <= 2048, "register file: 65536 = 32 lanes x 2048");
+constexpr int kCP1Regs = 80;
+constexpr int kCP2Regs = 72;   // launch allocation (no setmaxnreg)
+static_assert(8 * kCProdRegs + kCP1Warps * kCP1Regs + kCP2Warps * kCP2Regs <= 2048, "register file: 65536 = 32 lanes x 2048");
 #ifndef ZPC_COOP_POLY
 #define ZPC_COOP_POLY 0   // eighths of the pass-1 exp2 pairs computed on the FMA pipe instead of MUFU
 #endif
@@ -180,6 +181,7 @@ struct CfgC {
   static constexpr int W2 = W / 2;
   static constexpr int SLABS = D / 64;                 // 64-element (128 B) K-chunks
   static constexpr int KSTEPS = D / 16;
+  static constexpr int HALF = GWH / 2;                 // pass-2 B rows per CTA per column half (W/4 window rows)
   
   static constexpr uint32_t SLAB_Q = GWH * 128;        // GWH rows of 128 B; the pass-1 A operand reads 128
   static constexpr uint32_t Q_BYTES = SLAB_Q * SLABS;  // rows from a slab start (rows >= GWH: don't care)
@@ -281,7 +283,7 @@ __global__ void __launch_bounds__(kCThreads, 1) k_score_coop(Call c, CoopArgs a,
   // T, r, l, h, tb, unit (-1: no more chunks), ci, c, nt, slot
   volatile int* ctab = reinterpret_cast<volatile int*>(smem + K::OFF_SCHED + kDescRing * 4);
   const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + 8);
-  const uint32_t accf0 = smem_u32(bars + 16), acce0 = smem_u32(bars + 20);   // 0, 1: pass-1 buffers, 2: pass 2
+  const uint32_t accf0 = smem_u32(bars + 16), acce0 = smem_u32(bars + 20);   // 0, 1: pass-1 buffers, 2, 3: pass-2 halves
   const uint32_t qfull0 = smem_u32(bars + 24), qempty0 = smem_u32(bars + 27);
   const uint32_t augf0 = smem_u32(bars + 30), auge0 = smem_u32(bars + 32);
   const uint32_t p1pub0 = smem_u32(bars + 34);     // [4] pass-1 partials of chunk j stored (-> combiner)
@@ -300,7 +302,7 @@ __global__ void __launch_bounds__(kCThreads, 1) k_score_coop(Call c, CoopArgs a,
       mbar_init(full0 + 8 * s, kCLoadWarps * 32 + (rank == 0 ? 1 : 0));   // + rank 1's relay
       mbar_init(empty0 + 8 * s, 1);
     }
-    for (int i = 0; i < 3; ++i) { mbar_init(accf0 + 8 * i, 1); mbar_init(acce0 + 8 * i, i < 2 ? 2 * kCP1Warps : 2 * kCP2Warps); }
+    for (int i = 0; i < 4; ++i) { mbar_init(accf0 + 8 * i, 1); mbar_init(acce0 + 8 * i, i < 2 ? kCP1Warps : 2 * kCP2Warps); }
     for (int b = 0; b < kQBufs; ++b) { mbar_init(qfull0 + 8 * b, rank == 0 ? 2 : 1); mbar_init(qempty0 + 8 * b, 1); }
     for (int b = 0; b < 2; ++b) { mbar_init(augf0 + 8 * b, 2); mbar_init(auge0 + 8 * b, 1); }
     for (int b = 0; b < 4; ++b) mbar_init(p1pub0 + 8 * b, 1);
@@ -618,7 +620,8 @@ __global__ void __launch_bounds__(kCThreads, 1) k_score_coop(Call c, CoopArgs a,
       // descriptors come from the feeder (visible once the stage's full barrier completes)
       int n1 = 0, n2 = 0;
       const uint64_t aug_a = none_desc(smem_u32(smem + K::OFF_AUG_A), 128, 256);
-      constexpr uint32_t kId1 = idesc_bf16(256, kTile), kId2 = idesc_bf16(256, K::GW);
+      constexpr uint32_t kId1 = idesc_bf16(256, kTile), kId2 = idesc_bf16(256, K::GWH);
+      if (lane == 0) { CTRACE(49148, clk32()); CTRACE(49149, (uint32_t)gtime_ns()); }
       for (int g = 0;; ++g) {
         const int st = g % K::ST;
         if (g < 8192 && lane == 0) CTRACE(4 * g, clk32());
@@ -647,19 +650,28 @@ __global__ void __launch_bounds__(kCThreads, 1) k_score_coop(Call c, CoopArgs a,
             if (hs == 0 && g < 8192 && lane == 0) CTRACE(4 * g + 2, clk32());
           }
         } else {
+          // pass 2: two column halves (N = G*w/2: rows [h*HALF, +HALF) of each CTA's Q half and of B_aug),
+          // each into its own TMEM buffer (columns 256 + h*GWH), so the epilogue drains one while the
+          // tensor core fills the other
           const int ab = j & 1;
           if (dsc & 2u) mbar_wait_cluster(augf0 + 8 * ab, (uint32_t)((j >> 1) & 1));
-          mbar_wait_cluster(acce0 + 16, (n2 & 1) ^ 1);
-          if (g < 8192 && lane == 0) CTRACE(4 * g + 2, clk32());
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          tc_fence_after();
-          const uint64_t aug_b = none_desc(smem_u32(smem + K::OFF_AUG_B + ab * K::AUG_B_BYTES), 128, 256);
+#pragma unroll 1
+          for (int h = 0; h < 2; ++h) {
+            mbar_wait_cluster(acce0 + 8 * (2 + h), (n2 & 1) ^ 1);
+            if (h == 0 && g < 8192 && lane == 0) CTRACE(4 * g + 2, clk32());
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            tc_fence_after();
+            const uint64_t qdh = sw128_desc(smem_u32(smem + K::OFF_Q + qb * K::Q_BYTES) + h * K::HALF * 128);
+            const uint64_t aug_b =
+                none_desc(smem_u32(smem + K::OFF_AUG_B + ab * K::AUG_B_BYTES) + h * (K::HALF / 8) * 256, 128, 256);
+            const uint32_t dacc = tmem + 256 + h * K::GWH;
 #pragma unroll
-          for (int kk = 0; kk < K::KSTEPS; ++kk)
-            if (!CDEBUG(8)) umma2_elect(tmem + 256, kd0 + (((kk >> 2) * K::SLAB_K + (kk & 3) * 32) >> 4),
-                        qd + (((kk >> 2) * K::SLAB_Q + (kk & 3) * 32) >> 4), kId2, kk > 0);
-          if (!CDEBUG(8)) umma2_elect(tmem + 256, aug_a, aug_b, kId2, 1);
-          umma2_commit_elect(accf0 + 16);
+            for (int kk = 0; kk < K::KSTEPS; ++kk)
+              if (!CDEBUG(8)) umma2_elect(dacc, kd0 + (((kk >> 2) * K::SLAB_K + (kk & 3) * 32) >> 4),
+                                          qdh + (((kk >> 2) * K::SLAB_Q + (kk & 3) * 32) >> 4), kId2, kk > 0);
+            if (!CDEBUG(8)) umma2_elect(dacc, aug_a, aug_b, kId2, 1);
+            umma2_commit_elect(accf0 + 8 * (2 + h));
+          }
           ++n2;
           if (dsc & 4u) {
             umma2_commit_elect(auge0 + 8 * ab);        // B_aug[ab] free once this chunk's pass 2 is done
@@ -669,20 +681,24 @@ __global__ void __launch_bounds__(kCThreads, 1) k_score_coop(Call c, CoopArgs a,
         umma2_commit_elect(empty0 + 8 * st);
         if (g < 8192 && lane == 0) CTRACE(4 * g + 3, clk32());
       }
+      if (lane == 0) { CTRACE(49150, clk32()); CTRACE(49151, (uint32_t)gtime_ns()); }
     }
   } else if (warp < kCEpi0 + kCP1Warps) {
-    // ================= pass-1 warps (16): lane quarter q = local columns q*32 + lane; the four warps of a
-    // quarter take the four 32-token slices of each 128-token sub-step (slices 0, 1 = rank 0's K rows)
+    // ================= pass-1 warps (16): lane quarter q = local columns q*32 + lane. Warp tq of a quarter
+    // takes sub-step hs = tq >> 1 of every tile (buffer hs) and the 64 tokens of rank tq & 1 in it, so the
+    // two warp pairs of a quarter alternate buffers: while one pair computes, the MMA refills the other.
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kCP1Regs));
     const int q = warp & 3;
     const int tq = (warp - kCEpi0) >> 2;
+    const int hs = tq >> 1;
     const int lc = q * 32 + lane;
     const bool col_ok = lc < K::GWH;
     const bool warp_cols = q * 32 < K::GWH;
     const int gcol = rank * K::GWH + lc;
     const int u1 = col_ok ? gcol / G : 0;
-    const uint32_t tbase0 = tmem + ((uint32_t)(q * 32) << 16) + tq * 32;
-    constexpr int NB = 32;
-    int n1 = 0;
+    const uint32_t tbase0 = tmem + ((uint32_t)(q * 32) << 16) + hs * 128 + (tq & 1) * 64;
+    constexpr int NB = 64;
+    int n1 = 0;   // tiles processed
     for (int jp = 0;; ++jp) {
       mbar_wait(ctabf0 + 8 * (jp & 7), (uint32_t)((jp >> 3) & 1));
       Chunk A;
@@ -697,56 +713,54 @@ __global__ void __launch_bounds__(kCThreads, 1) k_score_coop(Call c, CoopArgs a,
       // token; a batch whose sum leaves [0, 2^100) -- a logit ~100 log2 units above the reference -- is
       // redone against its own maximum (rescaling the running sum), so no exponent can overflow
       float m = -INFINITY, ssum = 0.f;
-      for (int k = 0; k < A.nt; ++k) {
 #pragma unroll 1
-        for (int hs = 0; hs < 2; ++hs) {
-          const int ab = n1 & 1;
-          if (warp == kCEpi0 && lane == 0 && n1 < 1024) CTRACE(45056 + 4 * n1, clk32());
-          mbar_wait(accf0 + 8 * ab, (n1 >> 1) & 1);
-          if (warp == kCEpi0 && lane == 0 && n1 < 1024) CTRACE(45056 + 4 * n1 + 1, clk32());
-          tc_fence_after();
-          ++n1;
-          // first token of this warp's 32: rank (tq >> 1)'s K rows hs*64 + (tq & 1)*32 of the pair-tile
-          const int tb = (A.tb + k) * 2 * kTile + (tq >> 1) * kTile + hs * 64 + (tq & 1) * 32;
-          if (tb >= A.T || !warp_cols) {
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_remote_arrive_relaxed(acce0 + 8 * ab, 0);
-            continue;
-          }
-          float vp[NB];
-          TMEM_LD16(tbase0 + ab * 128, vp, 0);
-          TMEM_LD16(tbase0 + ab * 128 + 16, vp, 16);
-          tmem_wait_ld();
+      for (int k = 0; k < A.nt; ++k, ++n1) {
+        if (warp == kCEpi0 && lane == 0 && n1 < 1024) CTRACE(45056 + 4 * n1, clk32());
+        mbar_wait(accf0 + 8 * hs, (uint32_t)(n1 & 1));
+        if (warp == kCEpi0 && lane == 0 && n1 < 1024) CTRACE(45056 + 4 * n1 + 1, clk32());
+        tc_fence_after();
+        // first token of this warp's 64: rank (tq & 1)'s K rows hs*64 .. of the pair-tile
+        const int tb = (A.tb + k) * 2 * kTile + (tq & 1) * kTile + hs * 64;
+        if (tb >= A.T || !warp_cols) {
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_remote_arrive_relaxed(acce0 + 8 * ab, 0);
-          if (warp == kCEpi0 && lane == 0 && n1 <= 1024) CTRACE(45056 + 4 * (n1 - 1) + 2, clk32());
-          if (tb + NB - 1 > A.T - W) {
-#pragma unroll
-            for (int jj = 0; jj < NB; ++jj) vp[jj] = (tb + jj > limit1) ? -INFINITY : vp[jj];
-          }
-          auto vmax = [&](const float* v) {
-            float t3[10];
-#pragma unroll
-            for (int jj = 0; jj < 10; ++jj) t3[jj] = max3f(v[3 * jj], v[3 * jj + 1], v[3 * jj + 2]);
-            return fmaxf(max3f(max3f(t3[0], t3[1], t3[2]), max3f(t3[3], t3[4], t3[5]), max3f(t3[6], t3[7], t3[8])),
-                         max3f(t3[9], v[30], v[31]));
-          };
-          if (m == -INFINITY) m = vmax(vp) * scale;   // first batch of the chunk (or all masked so far)
-          if (CDEBUG(1)) { ssum += vp[0]; continue; }
-          if (m > -INFINITY) {
-            float bsum = coop_sum_exp<NB, ZPC_COOP_POLY>(vp, scale, m);
-            if (!(bsum < 0x1p100f)) {
-              const float mn = fmaxf(m, vmax(vp) * scale);
-              ssum *= ex2f(m - mn);
-              m = mn;
-              bsum = coop_sum_exp<NB, 0>(vp, scale, m);
-            }
-            ssum += bsum;
-          }
-          if (warp == kCEpi0 && lane == 0 && n1 <= 1024) CTRACE(45056 + 4 * (n1 - 1) + 3, __float_as_uint(ssum) == 1u ? 0u : clk32());
+          if (lane == 0) mbar_remote_arrive_relaxed(acce0 + 8 * hs, 0);
+          continue;
         }
+        float vp[NB];
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) TMEM_LD16(tbase0 + kk * 16, vp, kk * 16);
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_remote_arrive_relaxed(acce0 + 8 * hs, 0);
+        if (warp == kCEpi0 && lane == 0 && n1 < 1024) CTRACE(45056 + 4 * n1 + 2, clk32());
+        if (tb + NB - 1 > A.T - W) {
+#pragma unroll
+          for (int jj = 0; jj < NB; ++jj) vp[jj] = (tb + jj > limit1) ? -INFINITY : vp[jj];
+        }
+        auto vmax = [&](const float* v) {
+          float t3[21];
+#pragma unroll
+          for (int jj = 0; jj < 21; ++jj) t3[jj] = max3f(v[3 * jj], v[3 * jj + 1], v[3 * jj + 2]);
+          float r = v[63];
+#pragma unroll
+          for (int jj = 0; jj < 21; jj += 3) r = fmaxf(r, max3f(t3[jj], t3[jj + 1], t3[jj + 2]));
+          return r;
+        };
+        if (m == -INFINITY) m = vmax(vp) * scale;   // first batch of the chunk (or all masked so far)
+        if (CDEBUG(1)) { ssum += vp[0]; continue; }
+        if (m > -INFINITY) {
+          float bsum = coop_sum_exp<NB, ZPC_COOP_POLY>(vp, scale, m);
+          if (!(bsum < 0x1p100f)) {
+            const float mn = fmaxf(m, vmax(vp) * scale);
+            ssum *= ex2f(m - mn);
+            m = mn;
+            bsum = coop_sum_exp<NB, 0>(vp, scale, m);
+          }
+          ssum += bsum;
+        }
+        if (warp == kCEpi0 && lane == 0 && n1 < 1024) CTRACE(45056 + 4 * n1 + 3, __float_as_uint(ssum) == 1u ? 0u : clk32());
       }
       // ---- end of chunk A's pass 1: merge the four token slices (two rounds through smem) -> part
       auto merge = [&](float mo, float so) {
@@ -774,11 +788,13 @@ __global__ void __launch_bounds__(kCThreads, 1) k_score_coop(Call c, CoopArgs a,
   } else {
     // ================= pass-2 warps (4): token t = tile*256 + rank*128 + q*32 + lane, all window rows of
     // the pass-2 accumulator (B_aug already subtracted L2/s), in chunks of RC rows
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kCP2Regs));
     const int q = warp & 3;
     const uint32_t tbase2 = tmem + ((uint32_t)(q * 32) << 16) + 256;
-    constexpr int RC = G >= 7 ? 4 : 8;
-    constexpr int NCH = W / RC;
+    // half h (buffer 256 + h*GWH) holds, per token, window rows h*W/4 .. +W/4 (rank 0's Q rows) then
+    // W/2 + h*W/4 .. +W/4 (rank 1's)
+    constexpr int RQ = W / 4;
+    constexpr int RC = G >= 7 ? 4 : 8;   // rows per TMEM load chunk
+    static_assert(RQ % RC == 0, "chunking");
     int n2 = 0;
     for (int jq = 0;; ++jq) {
       mbar_wait(ctabf0 + 8 * (jq & 7), (uint32_t)((jq >> 3) & 1));
@@ -790,41 +806,46 @@ __global__ void __launch_bounds__(kCThreads, 1) k_score_coop(Call c, CoopArgs a,
         B.T = ce[0]; B.tb = ce[4]; B.nt = ce[8];
       }
       for (int k = 0; k < B.nt; ++k, ++n2) {
-        mbar_wait(accf0 + 16, n2 & 1);
-        tc_fence_after();
         const int t = (B.tb + k) * 2 * kTile + rank * kTile + q * 32 + lane;
         const int du = t - (B.T - W);   // window row u contributes iff u >= du (token t <= T-w+u)
         float acc[4] = {0.f, 0.f, 0.f, 0.f};
-        if (CDEBUG(2)) {   // bisection: no pass-2 math
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_remote_arrive_relaxed(acce0 + 16, 0);
-        } else
-#pragma unroll
-        for (int ch = 0; ch < NCH; ++ch) {
-          float v[RC * G];
-#pragma unroll
-          for (int kk = 0; kk < RC * G / 4; ++kk) TMEM_LD4(tbase2 + ch * RC * G + kk * 4, v, kk * 4);
-          tmem_wait_ld();
-          if (ch + 1 == NCH) {
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+          mbar_wait(accf0 + 8 * (2 + h), (uint32_t)(n2 & 1));
+          tc_fence_after();
+          if (CDEBUG(2)) {   // bisection: no pass-2 math
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_remote_arrive_relaxed(acce0 + 16, 0);
+            if (lane == 0) mbar_remote_arrive_relaxed(acce0 + 8 * (2 + h), 0);
+            continue;
           }
 #pragma unroll
-          for (int r = 0; r < RC; ++r) {
-            const float* y = v + r * G;
-            float mx;
-            if constexpr (G == 7) mx = max3f(max3f(y[0], y[1], y[2]), max3f(y[3], y[4], y[5]), y[6]);
-            else if constexpr (G == 8) mx = max3f(max3f(y[0], y[1], y[2]), max3f(y[3], y[4], y[5]), fmaxf(y[6], y[7]));
-            else if constexpr (G == 5) mx = max3f(max3f(y[0], y[1], y[2]), y[3], y[4]);
-            else {
-              mx = y[0];
+          for (int ch = 0; ch < 2 * RQ / RC; ++ch) {
+            float v[RC * G];
 #pragma unroll
-              for (int g = 1; g < G; ++g) mx = fmaxf(mx, y[g]);
+            for (int kk = 0; kk < RC * G / 4; ++kk) TMEM_LD4(tbase2 + h * K::GWH + ch * RC * G + kk * 4, v, kk * 4);
+            tmem_wait_ld();
+            if (ch + 1 == 2 * RQ / RC) {
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_remote_arrive_relaxed(acce0 + 8 * (2 + h), 0);
             }
-            const float pterm = ex2f(mx * scale);
-            acc[r & 3] += (ch * RC + r >= du) ? pterm : 0.f;
+            const int ubase = (ch * RC / RQ) * (W / 2) + h * RQ + (ch * RC) % RQ;
+#pragma unroll
+            for (int r = 0; r < RC; ++r) {
+              const float* y = v + r * G;
+              float mx;
+              if constexpr (G == 7) mx = max3f(max3f(y[0], y[1], y[2]), max3f(y[3], y[4], y[5]), y[6]);
+              else if constexpr (G == 8) mx = max3f(max3f(y[0], y[1], y[2]), max3f(y[3], y[4], y[5]), fmaxf(y[6], y[7]));
+              else if constexpr (G == 5) mx = max3f(max3f(y[0], y[1], y[2]), y[3], y[4]);
+              else {
+                mx = y[0];
+#pragma unroll
+                for (int g = 1; g < G; ++g) mx = fmaxf(mx, y[g]);
+              }
+              const float pterm = ex2f(mx * scale);
+              acc[r & 3] += (ubase + r >= du) ? pterm : 0.f;
+            }
           }
         }
         if (t < B.T)

@@ -44,6 +44,9 @@ wready = d(mma[:, 1], mma[:, 2])
 issue = d(mma[:, 2], mma[:, 3])
 gap = np.r_[0, d(mma[:-1, 3], top[1:])]
 total = d(top[0], mma[-1, 3])
+clk_span, ns_span = d(t[49148], t[49150]), d(t[49149], t[49151])
+if ns_span > 0:
+    print(f"pair 0 MMA loop: {clk_span} clk in {ns_span / 1e3:.1f} us -> SM clock {clk_span / ns_span:.3f} GHz")
 print(f"steps {n}  span {total} clk ({total / 1.9e3:.1f} us at 1.9 GHz)  per step {total / n:.0f} clk")
 for k, name in [(0, "pass1"), (1, "pass2")]:
     m = kind == k
