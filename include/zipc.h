@@ -22,7 +22,9 @@
  *
  * Conventions for every entry point:
  *   - All array pointers are caller-owned DEVICE memory unless the name says _host.
- *     The library allocates nothing, keeps no global state, never synchronises the stream.
+ *     The library allocates nothing, keeps no mutable global state (the only process-wide value is
+ *     the resolved cuTensorMapEncodeTiled driver entry point, written once, read-only after) and
+ *     never synchronises the stream; it reads no environment variables.
  *     Outputs are valid after the caller synchronises `stream` (a cudaStream_t; NULL = legacy).
  *   - Host-detectable errors (bad descriptor/params, workspace too small) return a negative
  *     ZPC_ERR_* and enqueue NOTHING.
@@ -44,13 +46,15 @@
 extern "C" {
 #endif
 
-#define ZPC_ABI_VERSION 3
+#define ZPC_ABI_VERSION 4
 
 /* ---- return / status codes ---- */
 #define ZPC_OK                  0
 #define ZPC_ERR_INVALID_ARG    -1   /* bad descriptor/params: even pool_kernel, w<1, n_max<2,
                                        unsupported head_dim/dtype, h_q not a multiple of h_kv,
                                        G*w > 256, max_seq_len above the select limit, NULL pointer,
+                                       a per-layer pool of >= 2^32 elements (N_total*b*h_kv*d; the
+                                       kernels use 32-bit offsets inside a layer), unknown variant bits,
                                        ZPC_F_REDUNDANCY with lambda < 0, tau <= 0, p outside [0,1],
                                        a non-finite value, or block_size > 32 unless bf16 with
                                        block_size a multiple of 16 up to 256, ZPC_F_GLOBAL_SCORE
@@ -68,6 +72,7 @@ extern "C" {
 #define ZPC_ERR_SEQ_TOO_LONG  -14   /* device: seq_len > params.max_seq_len */
 #define ZPC_ERR_BAD_SLOT      -15   /* device: q_slot outside [0, M) */
 #define ZPC_ERR_CAPACITY      -16   /* device: freed list or free stack would overflow */
+#define ZPC_ERR_NONFINITE     -17   /* device (ZPC_F_VALIDATE): a Q or K element the call reads is Inf/NaN */
 /* When several requests fail, *status is the error of the lowest-index failing request
  * (its first failing check in the order SLOT, SEQ_TOO_LONG, TABLE(stride), NOT_TRIGGERED,
  * TABLE(range), TABLE(dup), TABLE(prefix run), BUDGET); batch-level checks come after. */
@@ -78,7 +83,9 @@ extern "C" {
 
 /* ---- flags ---- */
 #define ZPC_F_PREFIX      1u  /* use ref_counts: leading blocks with ref > 1 are shared (§4.5) */
-#define ZPC_F_VALIDATE    2u  /* also reject duplicate block ids inside a table */
+#define ZPC_F_VALIDATE    2u  /* also reject duplicate block ids inside a table (ZPC_ERR_BAD_TABLE) and any
+                                 non-finite Q / K element the call reads (ZPC_ERR_NONFINITE; reads every
+                                 K row of the call once more) */
 #define ZPC_F_COUNT_MOVES 4u  /* count moved rows into the workspace counter (bytes accounting) */
 #define ZPC_F_SCORE_CUDACORE 8u /* force the CUDA-core scoring kernel even for bf16 (testing) */
 #define ZPC_F_REDUNDANCY 16u  /* NEXT-1: lightning redundancy score (§C.7) with the
@@ -99,6 +106,11 @@ extern "C" {
                                  two: S[t] = (1/w) sum_u max_g exp(q.k_t/sqrt(d) - LSE[u][g])
                                  (PAPER.md:409-411 with the normaliser given). Results equal the
                                  two-pass ones when the input is the exact normaliser. */
+
+#define ZPC_F_POOL_FIRST 128u /* MaxPool1D only at a request's FIRST compression (pooling at
+                                 every step hurts Qwen3-8B; the paper pools at the first compression only):
+                                 requests with is_compressed[r] != 0 select on the unpooled score. Needs
+                                 batch.is_compressed (as ZPC_F_GLOBAL_SCORE does). */
 
 /* Pool geometry: K, V [L][N_total][b][h_kv][d], Q [L][M][w][h_q][d].
  * Q row u of slot j holds the query of position T-w+u of the request bound to slot j (R3). */
@@ -130,7 +142,17 @@ typedef struct {
   float redundancy_p;
   /* ZPC_F_GLOBAL_SCORE only: decay alpha in [0, 1] (PAPER.md:441; 0.8 recommended, :718) */
   float global_alpha;
+  /* Kernel-variant overrides for tests and A/B timing (ZPC_V_*; 0 = automatic choice). Every variant
+   * computes the same result; only the launch configuration differs. */
+  uint32_t variant;
 } zpc_params;
+
+/* ---- zpc_params.variant ---- */
+#define ZPC_V_SCORE_SERIAL   1u        /* two-pass tcgen05 scoring: the per-unit serial kernel (k_score_tc)
+                                          instead of the cooperative / overlapped ones */
+#define ZPC_V_SELECT_SHIFT   4         /* bits 4..5: 0 auto, 1 k_select, 2 k_select_reg (T <= 32K) */
+#define ZPC_V_COMPACT_SHIFT  8         /* bits 8..10: 0 auto, 1..4 = k_compact CTA width 128/256/512/1024 */
+#define ZPC_V_MASK           0x733u
 
 #define ZPC_MAX_SEQ_LEN 49152   /* select keeps a unit's scores in shared memory */
 
@@ -173,6 +195,7 @@ typedef struct {
   int32_t* status;
   /* ZPC_F_GLOBAL_SCORE only (else ignored, may be NULL):
    *   global_scores  dev fp32 [L][N_total][b][h_kv], in/out: F, the global-score pool
+   * ZPC_F_GLOBAL_SCORE or ZPC_F_POOL_FIRST:
    *   is_compressed  dev int32 [R], 0 or 1: the request was compressed before (Alg. 2 line 3) */
   float* global_scores;
   const int32_t* is_compressed;

@@ -32,11 +32,13 @@ ERR_NO_FREE_BLOCKS = -13
 ERR_SEQ_TOO_LONG = -14
 ERR_BAD_SLOT = -15
 ERR_CAPACITY = -16
+ERR_NONFINITE = -17   # F_VALIDATE: a Q or K element the call reads is Inf/NaN (ABI-level check, R33)
 
 F_PREFIX = 1
 F_VALIDATE = 2
 F_REDUNDANCY = 16   # NEXT-1: lightning redundancy + temperature softmax + S - lambda*R
 F_GLOBAL_SCORE = 32  # NEXT-2: global score (Alg. 2) + F relocation with the kept rows
+F_POOL_FIRST = 128   # pool (MaxPool1D) only at a request's first compression (R32)
 
 
 @dataclass
@@ -410,9 +412,11 @@ def unit_keys(geo: Geometry, k_pool_f64, table, T: int, l: int, h: int) -> np.nd
 # and F keeps the updated, unpooled score; R27 an uncompressed request only stores S.
 # --------------------------------------------------------------------------
 def global_score_update(s: np.ndarray, f_layer: np.ndarray, table, T: int, h: int, b: int, n_max: int,
-                        compressed: bool, alpha: float) -> np.ndarray:
+                        compressed: bool, alpha: float, n_prefix: int = 0) -> np.ndarray:
     """Alg. 2 over the blocks of one unit, written out block by block. Mutates
-    f_layer ([N_total, b, h_kv] fp32) and returns the (possibly overwritten) scores."""
+    f_layer ([N_total, b, h_kv] fp32) and returns the (possibly overwritten) scores. R31: the F entries
+    of the request's shared prefix blocks (logical i < n_prefix) are read as history
+    but not written: the blocks belong to several requests."""
     s = s.copy()
     N = (T + b - 1) // b
     for i in range(N):
@@ -422,7 +426,8 @@ def global_score_update(s: np.ndarray, f_layer: np.ndarray, table, T: int, h: in
         if compressed and i < n_max - 1:                      # lines 6-8 (R25)
             fi = f_layer[p, :hi - lo, h].astype(np.float64)
             si = np.maximum(alpha * fi, si)
-        f_layer[p, :hi - lo, h] = si                          # lines 4 / 10 (fp32 store, R24)
+        if i >= n_prefix:
+            f_layer[p, :hi - lo, h] = si                      # lines 4 / 10 (fp32 store, R24; R31)
         if compressed:
             s[lo:hi] = si                                     # line 11
     return s
@@ -585,6 +590,20 @@ def compress(geo: Geometry, prm: Params, k_cache, v_cache, q_cache, q_slots, seq
     if pl.status != OK:
         return CompressOut(status=pl.status, plan=pl)
     R = len(seq_lens)
+    if prm.flags & F_VALIDATE:
+        # R33: every K row t < T of every unit and every window query row must be finite (the selection
+        # order of PAPER.md:591 is undefined for NaN scores); a batch-level check after plan's
+        kf_all, qf_all = widen(k_cache, geo.dtype), widen(q_cache, geo.dtype)
+        G = geo.h_q // geo.h_kv
+        for r in range(R):
+            T, tb = int(seq_lens[r]), np.asarray(tables[r])
+            t = np.arange(T)
+            for l in range(geo.L):
+                for h in range(geo.h_kv):
+                    rows = kf_all[l, tb[t // geo.b], t % geo.b, h]
+                    qw = qf_all[l, int(q_slots[r]), :, h * G:(h + 1) * G]
+                    if not (np.isfinite(rows).all() and np.isfinite(qw).all()):
+                        return CompressOut(status=ERR_NONFINITE, plan=pl)
     k_out = k_cache.copy()
     v_out = v_cache.copy()
     use_global = bool(prm.flags & F_GLOBAL_SCORE)
@@ -605,7 +624,8 @@ def compress(geo: Geometry, prm: Params, k_cache, v_cache, q_cache, q_slots, seq
                     if use_global:   # F is still updated by Alg. 2 before it is relocated
                         s = unit_scores(geo, qf, kf, tables[r], T, int(q_slots[r]), l, h, blockwise, window_lse_in)
                         gscores[key] = global_score_update(s, f_out[l], tables[r], T, h, geo.b, prm.n_max,
-                                                           bool(is_compressed[r]), prm.alpha)
+                                                           bool(is_compressed[r]), prm.alpha,
+                                                           int(pl.n_prefix[r]))
                 else:
                     if units is not None and key not in units:
                         continue
@@ -613,9 +633,11 @@ def compress(geo: Geometry, prm: Params, k_cache, v_cache, q_cache, q_slots, seq
                     scores[key] = s
                     if use_global:
                         s = global_score_update(s, f_out[l], tables[r], T, h, geo.b, prm.n_max,
-                                                bool(is_compressed[r]), prm.alpha)
+                                                bool(is_compressed[r]), prm.alpha, int(pl.n_prefix[r]))
                         gscores[key] = s
-                    sp = max_pool(s, prm.pool_kernel)
+                    # R32: with F_POOL_FIRST only a request's first compression pools
+                    first = not (prm.flags & F_POOL_FIRST) or not bool(is_compressed[r])
+                    sp = max_pool(s, prm.pool_kernel if first else 1)
                     if prm.flags & F_REDUNDANCY:
                         rr = lightning_redundancy_raw(unit_keys(geo, kf, tables[r], T, l, h), geo.b, prm.sim_p)
                         redund[key] = rr

@@ -249,11 +249,64 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize_tail(Call c) {
 
 }  // namespace
 
+// ZPC_F_VALIDATE: every Q and K element the call reads must be finite (PAPER.md:591 pins the window at
+// +inf and the selection orders finite scores; a NaN key or query would make that order undefined).
+// One CTA per (unit, 2048-token slab): the unit's K rows t < T through the block table and, in slab 0, its
+// G*w window query rows; 16-B vectors, exponent-all-ones test (bf16 0x7F80, fp32 0x7F800000). Runs after
+// plan; a failure sets *status = ZPC_ERR_NONFINITE only if plan left it OK (batch-level check after the
+// per-request ones), so every later stage returns at entry and nothing is mutated.
+constexpr int kValSlab = 2048;
+__global__ void __launch_bounds__(256) k_validate(Call c) {
+  if (*c.status != ZPC_OK) return;
+  const int unit = blockIdx.x;
+  const int h = unit % c.h_kv;
+  const int l = (unit / c.h_kv) % c.L;
+  const int r = unit / (c.h_kv * c.L);
+  const int T = c.seq_lens[r];
+  const int t0 = blockIdx.y * kValSlab;
+  if (t0 >= T) return;
+  const int esz = c.dtype == ZPC_BF16 ? 2 : 4;
+  const int vpr = c.d * esz / 16;                       // 16-B vectors per row
+  const uint4* K = reinterpret_cast<const uint4*>(c.k_cache);
+  const int32_t* table = c.tables + (size_t)r * c.table_stride;
+  auto bad = [&](uint4 v) -> bool {
+    if (esz == 2) {
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+      bool b = false;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) b |= ((w[i] & 0x7F80u) == 0x7F80u) | ((w[i] & 0x7F800000u) == 0x7F800000u);
+      return b;
+    }
+    return ((v.x & 0x7F800000u) == 0x7F800000u) | ((v.y & 0x7F800000u) == 0x7F800000u) |
+           ((v.z & 0x7F800000u) == 0x7F800000u) | ((v.w & 0x7F800000u) == 0x7F800000u);
+  };
+  bool found = false;
+  const int n = (min(T, t0 + kValSlab) - t0) * vpr;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int t = t0 + i / vpr, e = i % vpr;
+    found |= bad(K[kv_row(c, l, table[t / c.b], t % c.b, h) * esz / 16 + e]);
+  }
+  if (blockIdx.y == 0) {
+    const uint4* Q = reinterpret_cast<const uint4*>(c.q_cache);
+    const int slot = c.q_slots[r];
+    const int nq = c.w * c.G * vpr;
+    for (int i = threadIdx.x; i < nq; i += blockDim.x) {
+      const int row = i / vpr, e = i % vpr, u = row / c.G, g = row % c.G;
+      found |= bad(Q[q_row(c, l, slot, u, h * c.G + g) * esz / 16 + e]);
+    }
+  }
+  if (__syncthreads_or(found) && threadIdx.x == 0) atomicCAS(c.status, ZPC_OK, ZPC_ERR_NONFINITE);
+}
+
 cudaError_t launch_plan(const Call& c, cudaStream_t s) {
   if (c.ref_counts && (c.flags & ZPC_F_PREFIX))
     cudaMemsetAsync(c.ws.marks, 0, sizeof(int32_t) * (size_t)c.N_total, s);
   if (c.R > 0) k_plan_req<<<c.R, 256, 0, s>>>(c);
   k_plan_scan<<<1, kScanThreads, 0, s>>>(c);
+  if ((c.flags & ZPC_F_VALIDATE) && c.R > 0) {
+    const dim3 grid((unsigned)(c.R * c.L * c.h_kv), (unsigned)((c.max_seq_len + kValSlab - 1) / kValSlab));
+    k_validate<<<grid, 256, 0, s>>>(c);
+  }
   return cudaGetLastError();
 }
 

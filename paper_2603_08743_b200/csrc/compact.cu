@@ -127,17 +127,12 @@ cudaError_t launch_compact(const Call& c, cudaStream_t s) {
   //   paper_op 2 requests (576 units,  ~4 per SM): 0.373 / 0.266 / 0.219 / 0.230
   //   paper_op 4 requests (1152 units, ~8 per SM): 0.495 / 0.402 / 0.429 / 0.453
   //   qwen7b 64 requests  (7168 units, 48 per SM): 2.620 / 2.535 / 2.672 / 2.772
-  static int sms = 0;
-  if (sms == 0) {
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
-      sms = 148;
-  }
+  int dev = 0, sms = 0;   // queried per call (the current device's SM count; no cached state)
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+    return cudaErrorInvalidDevice;
   int nt = units >= sms * 6 ? 256 : (units >= sms * 3 ? 512 : 1024);
-  if (const char* e = getenv("ZPC_COMPACT_NT")) {
-    const int v = atoi(e);
-    if (v == 128 || v == 256 || v == 512 || v == 1024) nt = v;
-  }
+  const uint32_t vnt = (c.variant >> ZPC_V_COMPACT_SHIFT) & 7u;   // params.variant override (tests, A/B)
+  if (vnt != 0) nt = 64 << vnt;
 #define ZPC_COMPACT_CASE(VPR)                                                      \
   case VPR:                                                                       \
     if (nt == 128) k_compact<VPR, 1, 128, 16><<<units, 128, 0, s>>>(c);           \

@@ -37,7 +37,8 @@ struct Call {
   int32_t L, h_kv, h_q, G, d, b, N_total, M, w, dtype;
   int32_t n_max, pool_kernel, max_seq_len;
   uint32_t flags;
-  uint32_t debug;      // tuning/bisection switches (ZPC_SCORE_DEBUG), 0 in production
+  uint32_t debug;      // tuning/bisection switches (ZPC_SCORE_DEBUG, -DZPC_TUNING builds only), else 0
+  uint32_t variant;    // zpc_params.variant (ZPC_V_*)
   float red_lambda, red_tau, red_p;   // ZPC_F_REDUNDANCY parameters
   float global_alpha;                 // ZPC_F_GLOBAL_SCORE decay
   int32_t R, table_stride, free_capacity, freed_capacity;

@@ -87,7 +87,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_red_mma(Call c) {
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
       const int q = lane + 32 * v, row = q / CPR, ch = q % CPR;
-      *reinterpret_cast<int4*>(st + row * ROWB + ch * 16) = pre[v];
+      // slots >= T are zeroed, not just masked: a stale slot holding Inf/NaN would make 0 * NaN = NaN
+      *reinterpret_cast<int4*>(st + row * ROWB + ch * 16) = row < nvalid ? pre[v] : make_int4(0, 0, 0, 0);
     }
     __syncwarp();
     if (k + 1 < kBlocksPerWarp && jb + 1 < nb) fetch(jb + 1);

@@ -953,7 +953,7 @@ cudaError_t dispatch_coop(const Call& c, cudaStream_t s, bool* used) {
 // Others (single-pass ZPC_F_LSE_INPUT, w = 16, G = 4) fall through to launch_score_tc.
 cudaError_t launch_score_coop(const Call& c, cudaStream_t s, bool* used) {
   *used = false;
-  if (c.dtype != ZPC_BF16 || c.lse_in != nullptr || c.w != 32) return cudaSuccess;
+  if (c.dtype != ZPC_BF16 || c.lse_in != nullptr || c.w != 32 || (c.variant & ZPC_V_SCORE_SERIAL)) return cudaSuccess;
   if (c.d != 64 && c.d != 128) return cudaSuccess;
   if (c.b < 5) return cudaSuccess;   // a 128-token tile must span <= kMaxIds blocks
   if (c.G != 5 && c.G != 7 && c.G != 8) return cudaSuccess;

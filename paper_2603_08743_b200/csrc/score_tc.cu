@@ -1293,524 +1293,6 @@ __global__ void __launch_bounds__(kThreadsO, 1) k_score_ovl(Call c, const __grid
 }
 
 
-// ------------------------------------------------------------------ CTA-pair overlapped kernel
-// k_score_ovl's schedule (pass 1 of unit j interleaved with pass 2 of unit j-1) on a CTA pair with
-// tcgen05.mma.cta_group::2 (only rank 0 issues; each CTA supplies half of every operand):
-//  * each CTA holds the Q rows of HALF the window (rows u in [rank*w/2, rank*w/2 + w/2): window columns
-//    rank*GW/2 .. +GW/2, padded to 128 rows) and HALF of every 256-token tile (tokens rank*128 .. +127);
-//  * pass 1: M = 256 columns (A = Q halves), N = 128 tokens per sub-step (B = 64 K rows per CTA);
-//    each CTA's TMEM gets ITS columns over all 128 tokens, so a column's softmax normaliser is complete
-//    inside one CTA (no cluster exchange);
-//  * pass 2: M = 256 tokens (A = K halves), N = G*w columns (B = Q halves) + the B_aug K-step (each CTA
-//    supplies the -L2/s rows of its own columns); each CTA's TMEM gets ITS 128 tokens x all columns.
-// Per flop the tensor core reads half the shared-memory operand bytes of the one-CTA kernels (the
-// one-CTA pass-1 MMA with N = 64 was shared-memory-port bound), Q is half the size per CTA, and the K
-// ring has 4 stages. Cross-CTA handshakes: the MMA commits multicast to both CTAs' barriers; rank 1's
-// stage and Q completions are relayed to rank 0 (warp 2 / the Q producer), and both CTAs' epilogue
-// warps arrive on rank 0's accumulator-empty and B_aug-full barriers.
-template <int G, int W, int D>
-struct CfgP {
-  static constexpr int GW = G * W;
-  static constexpr int GWH = GW / 2;                   // columns per CTA
-  static constexpr int W2 = W / 2;                     // window rows per CTA
-  static constexpr int SLABS = D / 64;
-  static constexpr int KSTEPS = D / 16;
-  static constexpr int HC = (W / 2) * G;               // pass-2 columns per epilogue half
-  static constexpr uint32_t SLAB_Q = 128 * 128;        // 128 rows (GWH valid) of 128 B
-  static constexpr uint32_t Q_BYTES = SLAB_Q * SLABS;
-  static constexpr uint32_t Q_TX = GWH * 128 * SLABS;  // TMA bytes per CTA per unit
-  static constexpr uint32_t SLAB_K = 128 * 128;
-  static constexpr uint32_t STAGE_BYTES = 128 * D * 2;
-  static constexpr uint32_t AUG_A_BYTES = 128 * 32;
-  static constexpr uint32_t AUG_B_BYTES = 128 * 32;
-  static constexpr uint32_t OFF_Q0 = 0;
-  static constexpr uint32_t OFF_Q1 = Q_BYTES;
-  static constexpr uint32_t OFF_AUG_A = 2 * Q_BYTES;
-  static constexpr uint32_t OFF_AUG_B = OFF_AUG_A + AUG_A_BYTES;
-  static constexpr uint32_t AUG_END = (OFF_AUG_B + AUG_B_BYTES + 1023) / 1024 * 1024;
-  static constexpr uint32_t F_BYTES = (2 * 128 + 2 * 128) * 4;   // pm/ps[128] (X-warp merge), comb[2][128]
-  static constexpr uint32_t IDS_BYTES = kIdSlots * kMaxIds * 4;
-  static constexpr uint32_t BAR_BYTES = 40 * 8 + 16;
-  static constexpr uint32_t MISC = F_BYTES + IDS_BYTES + BAR_BYTES;
-  static constexpr int STAGES_FIT = (int)((227 * 1024 - 1024 - MISC - AUG_END) / STAGE_BYTES);
-  static constexpr int ST = STAGES_FIT > 6 ? 6 : STAGES_FIT;
-  static constexpr uint32_t OFF_K = AUG_END;
-  static constexpr uint32_t OFF_F = OFF_K + ST * STAGE_BYTES;
-  static constexpr uint32_t OFF_IDS = OFF_F + F_BYTES;
-  static constexpr uint32_t OFF_BAR = OFF_IDS + IDS_BYTES;
-  static constexpr uint32_t SMEM = OFF_BAR + BAR_BYTES + 1024;
-  static_assert(GWH <= 128 && GWH % 16 == 0, "a CTA's columns must fit the 128 TMEM lanes, UMMA N/2 % 8");
-  static_assert(W == 32 || W == 16, "epilogue batching assumes w = 32 or 16");
-  static_assert(ST >= 2 && ST <= 8, "K ring depth");
-};
-
-
-template <int G, int W, int D>
-__global__ void __launch_bounds__(kThreadsO, 1) k_score_pair(Call c, const __grid_constant__ CUtensorMap tmap_q) {
-  using K = CfgP<G, W, D>;
-  if (*c.status != ZPC_OK) return;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* Ks = smem + K::OFF_K;
-  float* pm = reinterpret_cast<float*>(smem + K::OFF_F);   // [128] X-warp (token half 1) partial max
-  float* ps = pm + 128;                                     // [128] partial sums
-  float* comb = ps + 128;                                   // [2][128] pass-2 half sums
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + K::OFF_BAR);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 40);
-  int* ids = reinterpret_cast<int*>(smem + K::OFF_IDS);
-  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + 8);
-  const uint32_t accf0 = smem_u32(bars + 16), acce0 = smem_u32(bars + 19);   // 0,1: pass-1 buffers, 2: pass 2
-  const uint32_t qfull0 = smem_u32(bars + 22), qempty0 = smem_u32(bars + 24);
-  const uint32_t augf = smem_u32(bars + 26), auge = smem_u32(bars + 27);
-
-  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
-  uint32_t rank_u;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank_u));
-  const int rank = (int)rank_u;
-  const int cluster_id = blockIdx.x / 2;
-  const int nclusters = gridDim.x / 2;
-  const int units = c.R * c.L * c.h_kv;
-  const int nu = units > cluster_id ? (units - cluster_id + nclusters - 1) / nclusters : 0;
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < K::ST; ++s) {
-      mbar_init(full0 + 8 * s, kLoadWarps * 32 + (rank == 0 ? 1 : 0));   // + rank 1's relay
-      mbar_init(empty0 + 8 * s, 1);
-    }
-    for (int a = 0; a < 3; ++a) { mbar_init(accf0 + 8 * a, 1); mbar_init(acce0 + 8 * a, 2 * kEpiWarps); }
-    for (int b = 0; b < 2; ++b) { mbar_init(qfull0 + 8 * b, rank == 0 ? 2 : 1); mbar_init(qempty0 + 8 * b, 1); }
-    mbar_init(augf, 2);
-    mbar_init(auge, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 0 && lane == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_q)));
-  {
-    uint4* aug = reinterpret_cast<uint4*>(smem + K::OFF_AUG_A);
-    for (int i = threadIdx.x; i < (int)((K::AUG_A_BYTES + K::AUG_B_BYTES) / 16); i += kThreadsO) {
-      uint4 v = make_uint4(0u, 0u, 0u, 0u);
-      if (i < (int)(K::AUG_A_BYTES / 16) && ((i >> 3) & 1) == 0) v = make_uint4(0x3F803F80u, 0x00003F80u, 0u, 0u);
-      aug[i] = v;
-    }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(kTmemCols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
-  }
-  tc_fence_before();
-  __syncthreads();
-  cluster_sync_all();
-  tc_fence_after();
-  const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
-  const float scale = kLog2e * rsqrtf((float)D);
-
-  struct UnitInfo { int r, l, h, T, slot, nt; };
-  auto unit_info = [&](int j) {
-    const int unit = cluster_id + j * nclusters;
-    UnitInfo u;
-    u.h = unit % c.h_kv;
-    u.l = (unit / c.h_kv) % c.L;
-    u.r = unit / (c.h_kv * c.L);
-    u.T = c.seq_lens[u.r];
-    u.slot = c.q_slots[u.r];
-    u.nt = (u.T + 2 * kTile - 1) / (2 * kTile);   // 256-token pair tiles
-    return u;
-  };
-  struct Cur { int j, k, sub, nA, nB; UnitInfo A, B; };
-  auto cur_init = [&](Cur& s) {
-    s.j = 0; s.k = 0; s.sub = 0; s.nB = 0; s.nA = 0;
-    if (nu > 0) { s.A = unit_info(0); s.nA = s.A.nt; }
-  };
-  auto cur_settle = [&](Cur& s) -> bool {
-    while (true) {
-      if (s.j > nu) return false;
-      if (s.k >= max(s.nA, s.nB)) {
-        if (++s.j > nu) return false;
-        s.B = s.A; s.nB = s.nA; s.nA = 0;
-        if (s.j < nu) { s.A = unit_info(s.j); s.nA = s.A.nt; }
-        s.k = 0; s.sub = 0;
-        continue;
-      }
-      if (s.sub == 0) { if (s.k < s.nA) return true; s.sub = 1; }
-      if (s.k < s.nB) return true;
-      s.sub = 0; ++s.k;
-    }
-  };
-  auto cur_advance = [](Cur& s) { if (s.sub == 0) s.sub = 1; else { s.sub = 0; ++s.k; } };
-  // this CTA's first token of the current step's tile (pass 1 ascending, pass 2 descending)
-  auto cur_t0 = [&](const Cur& s) {
-    const int p = s.sub == 0 ? s.k : s.B.nt - 1 - s.k;
-    return p * 2 * kTile + rank * kTile;
-  };
-
-  if (warp < kEpiWarp0) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kProdRegsO));
-    if (warp == 0) {
-      // ================= Q producer: this CTA's half of the window of unit j -> buffer j & 1
-      if (lane == 0) {
-        const uint64_t drop = policy_evict_first();
-        for (int j = 0; j < nu; ++j) {
-          const UnitInfo u = unit_info(j);
-          const int qb = j & 1;
-          mbar_wait_backoff(qempty0 + 8 * qb, ((j >> 1) & 1) ^ 1, 2000);
-          mbar_expect_tx(qfull0 + 8 * qb, K::Q_TX);
-          const uint32_t qdst = smem_u32(smem + (qb ? K::OFF_Q1 : K::OFF_Q0));
-          const int qrow = (u.l * c.M + u.slot) * W + rank * K::W2;
-          for (int sl = 0; sl < K::SLABS; ++sl)
-            tma_load_3d(qdst + sl * K::SLAB_Q, &tmap_q, sl * 64, u.h * G, qrow, qfull0 + 8 * qb, drop);
-          if (rank == 1) {   // relay: rank 0's MMA needs both halves
-            mbar_wait_backoff(qfull0 + 8 * qb, (j >> 1) & 1, 200);
-            mbar_remote_arrive(qfull0 + 8 * qb, 0);
-          }
-        }
-      }
-      __syncwarp();
-    } else if (warp == 2) {
-      // ================= rank 1: relay each landed K stage to rank 0's full barrier
-      if (rank == 1 && lane == 0) {
-        Cur s;
-        cur_init(s);
-        for (int g = 0; cur_settle(s); ++g, cur_advance(s)) {
-          mbar_wait(full0 + 8 * (g % K::ST), (g / K::ST) & 1);
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          mbar_remote_arrive(full0 + 8 * (g % K::ST), 0);
-        }
-      }
-      __syncwarp();
-    } else if (warp >= 4 && warp < 4 + kLoadWarps) {
-      // ---- K gather (as k_score_tc) of this CTA's 128 tokens of the step's tile
-      constexpr int CPR = D / 8;
-      constexpr int RPP = kLoadWarps * 32 / CPR;
-      static_assert(RPP % 8 == 0, "the per-thread SW128 swizzle term needs rows-per-pass % 8 == 0");
-      const int et = threadIdx.x - 4 * 32;
-      const int cr = et % CPR, rsub = et / CPR;
-      const uint32_t chunk_off = (uint32_t)(cr >> 3) * K::SLAB_K;
-      const uint16_t* Kg = reinterpret_cast<const uint16_t*>(c.k_cache);
-      const uint32_t ids_base = smem_u32(ids);
-      const bool b_pow2 = (c.b & (c.b - 1)) == 0;
-      const int b_log2 = 31 - __clz(c.b);
-      const uint32_t dst_thr = (uint32_t)rsub * 128u + (uint32_t)(((cr & 7) ^ (rsub & 7)) << 4) + chunk_off;
-      const uint32_t hD = (uint32_t)c.h_kv * D;
-      Cur s;
-      cur_init(s);
-      for (int ld_step = 0; cur_settle(s); ++ld_step, cur_advance(s)) {
-        const UnitInfo& u = s.sub ? s.B : s.A;
-        const int st = ld_step % K::ST;
-        const int t0 = cur_t0(s);
-        const int j0 = b_pow2 ? (t0 >> b_log2) : t0 / c.b;
-        const int T = u.T;
-        const uint16_t* lbase = Kg + (size_t)u.l * c.N_total * c.b * hD + (size_t)u.h * D + cr * 8;
-        const uint32_t dst0 = smem_u32(Ks + st * K::STAGE_BYTES) + dst_thr;
-        named_bar(4, kLoadWarps * 32 + 32);
-        const uint32_t sid = ids_base + (uint32_t)(ld_step % kIdSlots) * kMaxIds * 4;
-        if (c.b == 16) {
-          constexpr int RB = 16 / RPP;
-          constexpr int NBLK = kTile / 16;
-          const uint32_t qstride = (uint32_t)RPP * hD;
-          const uint32_t rbase = (uint32_t)rsub * hD;
-          int blk[NBLK];
-#pragma unroll
-          for (int jb = 0; jb < NBLK; ++jb) blk[jb] = lds_s32(sid + 4u * (uint32_t)jb);
-          if (t0 + kTile <= T) {
-#pragma unroll
-            for (int jb = 0; jb < NBLK; ++jb) {
-              uint32_t off = (uint32_t)blk[jb] * 16u * hD + rbase;
-#pragma unroll
-              for (int q = 0; q < RB; ++q, off += qstride)
-                cp_async16(dst0 + (uint32_t)((jb * 16 + q * RPP) * 128), lbase + off);
-            }
-          } else {
-#pragma unroll
-            for (int jb = 0; jb < NBLK; ++jb) {
-              uint32_t off = (uint32_t)blk[jb] * 16u * hD + rbase;
-#pragma unroll
-              for (int q = 0; q < RB; ++q, off += qstride)
-                if (t0 + jb * 16 + q * RPP + rsub < T)
-                  cp_async16(dst0 + (uint32_t)((jb * 16 + q * RPP) * 128), lbase + off);
-            }
-          }
-        } else {
-          uint32_t off[kTile / RPP];
-#pragma unroll
-          for (int k = 0; k < kTile / RPP; ++k) {
-            const int t = t0 + RPP * k + rsub;
-            const int jr = b_pow2 ? (t >> b_log2) : t / c.b;
-            const int blk = lds_s32(sid + 4u * (uint32_t)min(max(jr - j0, 0), kMaxIds - 1));
-            off[k] = ((uint32_t)blk * (uint32_t)c.b + (uint32_t)(t - jr * c.b)) * hD;
-          }
-#pragma unroll
-          for (int k = 0; k < kTile / RPP; ++k)
-            if (t0 + RPP * k + rsub < T) cp_async16(dst0 + (uint32_t)(RPP * k * 128), lbase + off[k]);
-        }
-        cp_async_arrive_noinc(full0 + 8 * st);
-      }
-    } else if (warp == 3) {
-      // ================= feeder: block ids of this CTA's 128 tokens, kIdAhead tiles ahead + stage release
-      Cur ls, ps_;
-      cur_init(ls);
-      cur_init(ps_);
-      const uint32_t ids_base = smem_u32(ids);
-      auto issue_ids = [&](int slot) {
-        if (cur_settle(ls)) {
-          const UnitInfo& u = ls.sub ? ls.B : ls.A;
-          const int t0 = cur_t0(ls);
-          if (t0 < u.T) {
-            const int j0 = t0 / c.b;
-            const int nb = (min(t0 + kTile, u.T) - 1) / c.b - j0 + 1;
-            if (lane < nb)
-              asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(ids_base + (uint32_t)(slot * kMaxIds + lane) * 4u),
-                           "l"(c.tables + (size_t)u.r * c.table_stride + j0 + lane) : "memory");
-          }
-          cur_advance(ls);
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-      };
-#pragma unroll 1
-      for (int k = 0; k < kIdAhead; ++k) issue_ids(k);
-      for (int g = 0; cur_settle(ps_); ++g, cur_advance(ps_)) {
-        issue_ids((g + kIdAhead) % kIdSlots);
-        if (g >= K::ST) {
-          if (lane == 0) mbar_wait(empty0 + 8 * (g % K::ST), ((g / K::ST) & 1) ^ 1);
-          __syncwarp();
-        }
-        asm volatile("cp.async.wait_group %0;" ::"n"(kIdAhead) : "memory");
-        named_bar(4, kLoadWarps * 32 + 32);
-      }
-      asm volatile("cp.async.wait_all;" ::: "memory");
-    } else if (warp == 1 && rank == 0) {
-      // ================= MMA issuer (rank 0 only; converged warp, elected lane issues)
-      int kstep = 0, n1 = 0, n2 = 0;
-      const uint64_t aug_a = none_desc(smem_u32(smem + K::OFF_AUG_A), 128, 256);
-      const uint64_t aug_b = none_desc(smem_u32(smem + K::OFF_AUG_B), 128, 256);
-      const uint64_t qd0 = sw128_desc(smem_u32(smem + K::OFF_Q0));
-      const uint64_t qd1 = sw128_desc(smem_u32(smem + K::OFF_Q1));
-      constexpr uint32_t kId1 = idesc_bf16(256, kTile), kId2 = idesc_bf16(256, K::GW);
-      int nA = 0, nB = 0;
-      for (int j = 0; j <= nu; ++j) {
-        nB = nA;
-        nA = 0;
-        if (j < nu) nA = __shfl_sync(0xffffffffu, unit_info(j).nt, 0);
-        const uint64_t qdA = (j & 1) ? qd1 : qd0, qdB = (j & 1) ? qd0 : qd1;
-        bool q_ok = j >= nu, aug_ok = j == 0;
-        if (!q_ok && nA == 0) { mbar_wait_cluster(qfull0 + 8 * (j & 1), (j >> 1) & 1); q_ok = true; }
-        if (!aug_ok && nB == 0) { mbar_wait_cluster(augf, (j - 1) & 1); aug_ok = true; }
-        const int np = max(nA, nB);
-        for (int k = 0; k < np; ++k) {
-#pragma unroll 1
-          for (int sub = 0; sub < 2; ++sub) {
-            if (sub == 0 ? k >= nA : k >= nB) continue;
-            const int s = kstep % K::ST;
-            if (!(c.debug & 2048u)) mbar_wait_cluster(full0 + 8 * s, (kstep / K::ST) & 1);
-            if (sub == 0 && !q_ok) { mbar_wait_cluster(qfull0 + 8 * (j & 1), (j >> 1) & 1); q_ok = true; }
-            if (sub == 1 && !aug_ok) { mbar_wait_cluster(augf, (j - 1) & 1); aug_ok = true; }
-            const uint64_t kd0 = sw128_desc(smem_u32(Ks + s * K::STAGE_BYTES));
-            if (sub == 0) {
-              // pass 1: two sub-steps of N = 128 tokens (64 K rows from each CTA)
-#pragma unroll 1
-              for (int hs = 0; hs < 2; ++hs, ++n1) {
-                const int a = n1 & 1;
-                mbar_wait_cluster(acce0 + 8 * a, ((n1 >> 1) & 1) ^ 1);
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                tc_fence_after();
-                if (!(c.debug & 4u)) {
-#pragma unroll
-                  for (int kk = 0; kk < K::KSTEPS; ++kk)
-                    umma2_elect(tmem + a * 128, qdA + (((kk >> 2) * K::SLAB_Q + (kk & 3) * 32) >> 4),
-                                kd0 + (((kk >> 2) * K::SLAB_K + hs * 64 * 128 + (kk & 3) * 32) >> 4), kId1, kk > 0);
-                }
-                umma2_commit_elect(accf0 + 8 * a);
-              }
-            } else {
-              mbar_wait_cluster(acce0 + 16, (n2 & 1) ^ 1);
-              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-              tc_fence_after();
-              if (!(c.debug & 4u)) {
-#pragma unroll
-                for (int kk = 0; kk < K::KSTEPS; ++kk)
-                  umma2_elect(tmem + 256, kd0 + (((kk >> 2) * K::SLAB_K + (kk & 3) * 32) >> 4),
-                              qdB + (((kk >> 2) * K::SLAB_Q + (kk & 3) * 32) >> 4), kId2, kk > 0);
-                umma2_elect(tmem + 256, aug_a, aug_b, kId2, 1);
-              }
-              umma2_commit_elect(accf0 + 16);
-              ++n2;
-            }
-            umma2_commit_elect(empty0 + 8 * s);
-            ++kstep;
-          }
-        }
-        if (j > 0) {
-          umma2_commit_elect(auge);
-          umma2_commit_elect(qempty0 + 8 * ((j - 1) & 1));
-        }
-      }
-    }
-  } else if (warp < kEpiWarp0 + 8) {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kP1RegsO));
-    // ================= pass-1 warps (8): lane quarter q = local columns q*32 + lane; the two warps of a
-    // quarter take the two 64-token halves of each 128-token sub-step (half 0 = rank 0's K rows)
-    const int ew = warp - kEpiWarp0;
-    const int q = warp & 3;
-    const int half = ew >> 2;
-    const int lc = q * 32 + lane;
-    const bool col_ok = lc < K::GWH;
-    const int gcol = rank * K::GWH + lc;
-    const int u1 = col_ok ? gcol / G : 0;
-    const uint32_t tbase0 = tmem + ((uint32_t)(q * 32) << 16) + half * 64;
-    int n1 = 0;
-    for (int j = 0; j < nu; ++j) {
-      const UnitInfo A = unit_info(j);
-      const int unitA = cluster_id + j * nclusters;
-      const int limit1 = A.T - W + u1;
-      float m = -INFINITY, ssum = 0.f, m1 = -INFINITY, s1 = 0.f;
-      for (int k = 0; k < A.nt; ++k) {
-#pragma unroll 1
-        for (int hs = 0; hs < 2; ++hs) {
-          const int a = n1 & 1;
-          mbar_wait(accf0 + 8 * a, (n1 >> 1) & 1);
-          tc_fence_after();
-          ++n1;
-          const int tb = k * 2 * kTile + half * kTile + hs * 64;   // first token of this warp's 64
-          if ((c.debug & 2u) || tb >= A.T) {
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_remote_arrive_relaxed(acce0 + 8 * a, 0);
-            continue;
-          }
-          constexpr int NB = 32;
-          float vp[2 * NB];
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk) TMEM_LD16(tbase0 + a * 128 + kk * 16, vp, kk * 16);
-          tmem_wait_ld();
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_remote_arrive_relaxed(acce0 + 8 * a, 0);
-          if (tb + 2 * NB - 1 > A.T - W) {
-#pragma unroll
-            for (int jj = 0; jj < 2 * NB; ++jj) vp[jj] = (tb + jj > limit1) ? -INFINITY : vp[jj];
-          }
-          auto online = [&](const float* v, float& mm, float& ss) {
-            float t3[11];
-#pragma unroll
-            for (int jj = 0; jj < 10; ++jj) t3[jj] = max3f(v[3 * jj], v[3 * jj + 1], v[3 * jj + 2]);
-            t3[10] = fmaxf(v[30], v[31]);
-            const float mx = fmaxf(max3f(max3f(t3[0], t3[1], t3[2]), max3f(t3[3], t3[4], t3[5]),
-                                         max3f(t3[6], t3[7], t3[8])),
-                                   fmaxf(t3[9], t3[10]));
-            const float mn = fmaxf(mm, mx * scale);
-            const float mref = mn > -INFINITY ? mn : 0.f;
-            const float rescale = ex2f(mm - mref);
-            const float bsum = sum_exp_n<NB>(v, scale, mref);
-            ss = ss * rescale + bsum;
-            mm = mn;
-          };
-          online(vp, m, ssum);
-          online(vp + NB, m1, s1);
-        }
-      }
-      // ---- end of unit A's pass 1: merge the two streams, then the two token halves (smem)
-      {
-        const float mm = fmaxf(m, m1);
-        const float mr = mm > -INFINITY ? mm : 0.f;
-        ssum = ssum * ex2f(m - mr) + s1 * ex2f(m1 - mr);
-        m = mm;
-      }
-      if (half == 1) { pm[lc] = m; ps[lc] = ssum; }
-      named_bar(1, 8 * 32);
-      if (half == 0) {
-        const float mo = pm[lc], so = ps[lc];
-        const float mm = fmaxf(m, mo);
-        const float mr = mm > -INFINITY ? mm : 0.f;
-        const float S = ssum * ex2f(m - mr) + so * ex2f(mo - mr);
-        const float L2 = mm + lg2f(S);
-        mbar_wait(auge, (j & 1) ^ 1);   // pass-2 MMAs of unit j-1 (the last readers of B_aug) done
-        if (col_ok) {
-          const float nv = -L2 / scale;
-          const __nv_bfloat16 hi = __float2bfloat16_rn(nv);
-          const float r1 = nv - __bfloat162float(hi);
-          const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
-          const __nv_bfloat16 lo = __float2bfloat16_rn(r1 - __bfloat162float(mid));
-          const uint32_t w0 = (uint32_t)__bfloat16_as_ushort(hi) | ((uint32_t)__bfloat16_as_ushort(mid) << 16);
-          const uint32_t w1 = (uint32_t)__bfloat16_as_ushort(lo);
-          *reinterpret_cast<uint2*>(smem + K::OFF_AUG_B + (lc >> 3) * 256 + (lc & 7) * 16) = make_uint2(w0, w1);
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          c.ws.lse[(size_t)unitA * K::GW + gcol] = L2;
-        }
-      }
-      named_bar(1, 8 * 32);
-      if (ew == 0 && lane == 0) {
-        asm volatile("fence.acq_rel.cluster;" ::: "memory");
-        mbar_remote_arrive(augf, 0);
-      }
-    }
-  } else {
-    // ================= pass-2 warps (8): token t = tile*256 + rank*128 + q*32 + lane, window rows
-    // [half*W/2, half*W/2 + W/2) of accumulator 2 (B_aug already subtracted L2/s)
-    const int ew = warp - kEpiWarp0 - 8;
-    const int q = warp & 3;
-    const int half = ew >> 2;
-    const uint32_t tbase2 = tmem + ((uint32_t)(q * 32) << 16) + 256 + half * K::HC;
-    constexpr int RC = G >= 7 ? 4 : 8;
-    constexpr int NCH = (W / 2) / RC;
-    int n2 = 0;
-    for (int j = 0; j < nu; ++j) {
-      const UnitInfo B = unit_info(j);
-      const int unitB = cluster_id + j * nclusters;
-      for (int k = 0; k < B.nt; ++k, ++n2) {
-        mbar_wait(accf0 + 16, n2 & 1);
-        tc_fence_after();
-        const int t = (B.nt - 1 - k) * 2 * kTile + rank * kTile + q * 32 + lane;
-        const int du = t - (B.T - W) - half * (W / 2);
-        float acc[4] = {0.f, 0.f, 0.f, 0.f};
-        if (c.debug & 2u) {
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_remote_arrive_relaxed(acce0 + 16, 0);
-          continue;
-        }
-#pragma unroll
-        for (int ch = 0; ch < NCH; ++ch) {
-          float v[RC * G];
-#pragma unroll
-          for (int kk = 0; kk < RC * G / 4; ++kk) TMEM_LD4(tbase2 + ch * RC * G + kk * 4, v, kk * 4);
-          tmem_wait_ld();
-          if (ch + 1 == NCH) {
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_remote_arrive_relaxed(acce0 + 16, 0);
-          }
-#pragma unroll
-          for (int r = 0; r < RC; ++r) {
-            const float* y = v + r * G;
-            float mx;
-            if constexpr (G == 7) mx = max3f(max3f(y[0], y[1], y[2]), max3f(y[3], y[4], y[5]), y[6]);
-            else if constexpr (G == 8) mx = max3f(max3f(y[0], y[1], y[2]), max3f(y[3], y[4], y[5]), fmaxf(y[6], y[7]));
-            else {
-              mx = y[0];
-#pragma unroll
-              for (int g = 1; g < G; ++g) mx = fmaxf(mx, y[g]);
-            }
-            const float pterm = ex2f(mx * scale);
-            acc[r & 3] += (ch * RC + r >= du) ? pterm : 0.f;
-          }
-        }
-        const float accs = (acc[0] + acc[1]) + (acc[2] + acc[3]);
-        float* cb = comb + (n2 & 1) * kTile;
-        if (half == 1) cb[q * 32 + lane] = accs;
-        named_bar(2, 8 * 32);
-        if (half == 0 && t < B.T)
-          c.ws.scores[(size_t)unitB * c.max_seq_len + t] = (accs + cb[q * 32 + lane]) * (1.0f / W);
-      }
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  cluster_sync_all();   // the peer's MMAs / remote arrivals are over before TMEM is released
-  tc_fence_after();
-  if (warp == 1)
-    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
-}
-
 // ------------------------------------------------------------------ host side
 
 template <int G, int W, int D, int C, bool OVL>
@@ -1845,77 +1327,29 @@ cudaError_t launch_tc(const Call& c, const CUtensorMap& tq, cudaStream_t s) {
   return cudaLaunchKernelEx(&cfg, kern, c, tq);
 }
 
-// CTA-pair kernel (k_score_pair): G*w/2 >= 112 columns per CTA (G = 7, and G = 8 with w = 32), two-pass
-// calls, d = 128. Opt-in (ZPC_SCORE_PAIR=1): measured slower than k_score_ovl on the 7B batch (8.29 vs
-// 7.77 ms) -- it halves the tensor core's shared-memory reads, but the step is bound by the
-// pass-2 K re-read (HBM), and the pair adds cross-SM handshakes per sub-step.
-bool use_pair(const Call& c) {
-  if (c.lse_in != nullptr || c.w != 32 || c.d != 128 || (c.G != 7 && c.G != 8)) return false;
-  const char* e = getenv("ZPC_SCORE_PAIR");
-  return e != nullptr && atoi(e) != 0;
-}
-
-template <int G, int W, int D>
-cudaError_t launch_pair(const Call& c, cudaStream_t s) {
-  using K = CfgP<G, W, D>;
-  EncodeTiledFn enc = encode_fn();
-  if (!enc) return cudaErrorNotSupported;
-  // Q cache viewed as [rows = L*M*w][h_q][d]; one box = the unit's G heads x w/2 window rows (a CTA's half)
-  CUtensorMap tq;
-  const cuuint32_t estr[3] = {1, 1, 1};
-  const cuuint64_t qdim[3] = {(cuuint64_t)c.d, (cuuint64_t)c.h_q, (cuuint64_t)c.L * c.M * c.w};
-  const cuuint64_t qstr[2] = {(cuuint64_t)c.d * 2, (cuuint64_t)c.h_q * c.d * 2};
-  const cuuint32_t qbox[3] = {64, (cuuint32_t)G, (cuuint32_t)(W / 2)};
-  if (enc(&tq, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(c.q_cache), qdim, qstr, qbox, estr,
-          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-    return cudaErrorInvalidValue;
-  auto kern = k_score_pair<G, W, D>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K::SMEM);
-  if (e != cudaSuccess) return e;
-  const int units = c.R * c.L * c.h_kv;
-  cudaLaunchConfig_t cfg = {};
-  cfg.blockDim = dim3(kThreadsO);
-  cfg.dynamicSmemBytes = K::SMEM;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int max_clusters = sms / 2;
-  cfg.gridDim = dim3(2);
-  int q = 0;
-  if (cudaOccupancyMaxActiveClusters(&q, kern, &cfg) == cudaSuccess && q > 0) max_clusters = q;
-  cudaGetLastError();
-  cfg.gridDim = dim3((unsigned)(std::min(units, max_clusters) * 2));
-  return cudaLaunchKernelEx(&cfg, kern, c, tq);
-}
-
 // Cluster size: CTAs per unit. Splitting a unit's tokens over C CTAs shrinks the K slice each
 // CTA re-reads in pass 2 (in flight across the GPU: ~148/C slices), keeping it L2-resident
-// (DESIGN.md §Score kernel, L2 reuse). ZPC_SCORE_CLUSTER (1/2/4/8) overrides, for tuning runs.
+// (DESIGN.md §Score kernel, L2 reuse). Tuning builds (-DZPC_TUNING) read ZPC_SCORE_CLUSTER (1/2/4/8).
 int cluster_size(const Call& c) {
+#ifdef ZPC_TUNING
   if (const char* e = getenv("ZPC_SCORE_CLUSTER")) {
     const int v = atoi(e);
     if (v == 1 || v == 2 || v == 4 || v == 8) return v;
   }
+#endif
   return c.max_seq_len < 2 * kTile ? 1 : 2;
 }
 
 // Two-pass calls use the overlapped kernel (pass 1 of unit j || pass 2 of unit j-1); single-pass
 // calls (ZPC_F_LSE_INPUT) have no pass 1 to overlap and keep k_score_tc's deeper K ring.
-// ZPC_SCORE_OVL=0 selects k_score_tc for two-pass calls too (same-box A/B runs).
+// Tuning builds read ZPC_SCORE_OVL=0 to select k_score_tc for two-pass calls too (same-box A/B runs).
 bool use_ovl(const Call& c) {
   // w = 16 (the paper's b = 256 operating point, ~16 units per cluster per call): measured faster
   // serial (0.34 vs 0.46 ms per 4-request call), the interleave's start/drain is not amortised
-  if (c.lse_in != nullptr || c.w == 16) return false;
+  if (c.lse_in != nullptr || c.w == 16 || (c.variant & ZPC_V_SCORE_SERIAL)) return false;
+#ifdef ZPC_TUNING
   if (const char* e = getenv("ZPC_SCORE_OVL")) return atoi(e) != 0;
+#endif
   return true;
 }
 
@@ -1931,11 +1365,14 @@ cudaError_t launch_o(const Call& c, const CUtensorMap& tq, cudaStream_t s) {
   return cluster_size(c) >= 2 ? launch_tc<G, W, D, 2, OVL>(c, tq, s) : launch_tc<G, W, D, 1, OVL>(c, tq, s);
 }
 
-template <int G, int W, int D>
+// OVL_OK: the overlapped two-pass instance exists for this shape. Two-pass w = 32 calls with G = 5, 7, 8
+// are taken by the cooperative kernel (score_coop.cu) before this dispatcher; they arrive here only as
+// single-pass (ZPC_F_LSE_INPUT) calls.
+template <int G, int W, int D, bool OVL_OK>
 cudaError_t launch_c(const Call& c, const CUtensorMap& tq, cudaStream_t s) {
-  if constexpr (W == 32 && D == 128 && (G == 7 || G == 8))
-    if (use_pair(c)) return launch_pair<G, W, D>(c, s);
-  return use_ovl(c) ? launch_o<G, W, D, true>(c, tq, s) : launch_o<G, W, D, false>(c, tq, s);
+  if constexpr (OVL_OK)
+    if (use_ovl(c)) return launch_o<G, W, D, true>(c, tq, s);
+  return launch_o<G, W, D, false>(c, tq, s);
 }
 
 template <int D>
@@ -1944,18 +1381,18 @@ cudaError_t dispatch_g(const Call& c, const CUtensorMap& tq, cudaStream_t s, boo
     // the paper's own operating point (w = 16): Qwen3-8B / DS-Llama-8B (G = 4), 32B (G = 8)
     *used = true;
     switch (c.G) {
-      case 4: return launch_c<4, 16, D>(c, tq, s);
-      case 8: return launch_c<8, 16, D>(c, tq, s);
+      case 4: return launch_c<4, 16, D, false>(c, tq, s);
+      case 8: return launch_c<8, 16, D, false>(c, tq, s);
       default: *used = false; return cudaSuccess;
     }
   }
   if (c.w != 32) return cudaSuccess;
   *used = true;
   switch (c.G) {
-    case 4: return launch_c<4, 32, D>(c, tq, s);
-    case 5: return launch_c<5, 32, D>(c, tq, s);
-    case 7: return launch_c<7, 32, D>(c, tq, s);
-    case 8: return launch_c<8, 32, D>(c, tq, s);
+    case 4: return launch_c<4, 32, D, true>(c, tq, s);
+    case 5: return launch_c<5, 32, D, false>(c, tq, s);
+    case 7: return launch_c<7, 32, D, false>(c, tq, s);
+    case 8: return launch_c<8, 32, D, false>(c, tq, s);
     default: *used = false; return cudaSuccess;
   }
 }
@@ -1965,7 +1402,9 @@ cudaError_t dispatch_g(const Call& c, const CUtensorMap& tq, cudaStream_t s, boo
 cudaError_t launch_score_tc(const Call& c_in, cudaStream_t s, bool* used) {
   *used = false;
   Call c = c_in;
-  if (const char* e = getenv("ZPC_SCORE_DEBUG")) c.debug = (uint32_t)strtoul(e, nullptr, 10);   // tuning runs only
+#ifdef ZPC_TUNING   // bisection switches; the production library reads no environment
+  if (const char* e = getenv("ZPC_SCORE_DEBUG")) c.debug = (uint32_t)strtoul(e, nullptr, 10);
+#endif
   if (c.dtype != ZPC_BF16) return cudaSuccess;
   if (c.d != 64 && c.d != 128) return cudaSuccess;
   if (c.b < 5) return cudaSuccess;   // a 128-token tile must span <= kMaxIds blocks

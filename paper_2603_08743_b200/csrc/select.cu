@@ -89,7 +89,8 @@ __global__ void __launch_bounds__(kThreads) k_select(Call c) {
   const int ell = min(T, c.budgets[unit]);
   if (threadIdx.x == 0) c.new_lens[unit] = ell;
   const float* S = c.ws.scores + (size_t)unit * c.max_seq_len;
-  const int half = c.pool_kernel / 2;
+  // R32: ZPC_F_POOL_FIRST pools only a request's first compression
+  const int half = ((c.flags & ZPC_F_POOL_FIRST) && c.is_compressed[r]) ? 0 : c.pool_kernel / 2;
 
   // NEXT-2 (ZPC_F_GLOBAL_SCORE): Alg. 2 over the unit's blocks before pooling
   // (PAPER.md:487): F <- S for a request never compressed; otherwise S <- max(alpha F, S) on the
@@ -99,12 +100,15 @@ __global__ void __launch_bounds__(kThreads) k_select(Call c) {
     const int32_t* table = c.tables + (size_t)r * c.table_stride;
     float* Sw = c.ws.scores + (size_t)unit * c.max_seq_len;
     const size_t fplane = (size_t)l * c.N_total * c.b * c.h_kv + h;
+    // R31: F of the shared prefix blocks (logical < n_prefix) is history only, never stored (several
+    // requests of the batch own the block; their updates would race)
+    const int npre = (c.flags & ZPC_F_PREFIX) ? c.ws.n_prefix[r] : 0;
     for (int t = threadIdx.x; t < T; t += kThreads) {
       const int i = t / c.b;
       float* fp = c.f_cache + fplane + ((size_t)table[i] * c.b + (t - i * c.b)) * c.h_kv;
       float v = Sw[t];
       if (comp && i < c.n_max - 1) v = fmaxf(c.global_alpha * *fp, v);
-      *fp = v;
+      if (i >= npre) *fp = v;
       if (comp) Sw[t] = v;
     }
     __syncthreads();
@@ -283,7 +287,8 @@ __global__ void __launch_bounds__(NT) k_select_reg(Call c) {
   const int T = c.seq_lens[r];
   const int ell = min(T, c.budgets[unit]);
   if (threadIdx.x == 0) c.new_lens[unit] = ell;
-  const int half = c.pool_kernel / 2;
+  // R32: ZPC_F_POOL_FIRST pools only a request's first compression
+  const int half = ((c.flags & ZPC_F_POOL_FIRST) && c.is_compressed[r]) ? 0 : c.pool_kernel / 2;
 
   // NEXT-2 (ZPC_F_GLOBAL_SCORE): Alg. 2 as in k_select (R25-R27), S updated in place
   float* Sw = c.ws.scores + (size_t)unit * c.max_seq_len;
@@ -291,12 +296,13 @@ __global__ void __launch_bounds__(NT) k_select_reg(Call c) {
     const bool comp = c.is_compressed[r] != 0;
     const int32_t* table = c.tables + (size_t)r * c.table_stride;
     const size_t fplane = (size_t)l * c.N_total * c.b * c.h_kv + h;
+    const int npre = (c.flags & ZPC_F_PREFIX) ? c.ws.n_prefix[r] : 0;   // R31: shared blocks' F read only
     for (int t = threadIdx.x; t < T; t += NT) {
       const int i = t / c.b;
       float* fp = c.f_cache + fplane + ((size_t)table[i] * c.b + (t - i * c.b)) * c.h_kv;
       float v = Sw[t];
       if (comp && i < c.n_max - 1) v = fmaxf(c.global_alpha * *fp, v);
-      *fp = v;
+      if (i >= npre) *fp = v;
       if (comp) Sw[t] = v;
     }
     __syncthreads();
@@ -442,10 +448,10 @@ __global__ void __launch_bounds__(NT) k_select_reg(Call c) {
 cudaError_t launch_select(const Call& c, cudaStream_t s) {
   const int units = c.R * c.L * c.h_kv;
   if (units == 0) return cudaSuccess;
-  // register-resident variant while a thread's chunk fits CH <= 32 keys. ZPC_SELECT_REG (tests and A/B
-  // runs): 0 = always k_select, 2 = k_select_reg for every T <= 32K, unset/1 = by T as below
-  const char* e = getenv("ZPC_SELECT_REG");
-  const int mode = e ? atoi(e) : 1;
+  // register-resident variant while a thread's chunk fits CH <= 32 keys. params.variant (tests and A/B
+  // runs): select 1 = always k_select, 2 = k_select_reg for every T <= 32K, 0 = by T as below
+  const int vsel = (int)((c.variant >> ZPC_V_SELECT_SHIFT) & 3u);
+  const int mode = vsel == 0 ? 1 : (vsel == 1 ? 0 : 2);
   const bool reg = mode != 0;
   const int T = c.max_seq_len;
   // T <= 4K (the paper's operating point, T = 2304): k_select measured faster (0.066 ms per 4-request

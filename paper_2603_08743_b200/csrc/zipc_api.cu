@@ -21,6 +21,8 @@ bool desc_ok(const zpc_cache_desc* d, const zpc_params* p) {
   if (d->dtype != ZPC_BF16 && d->dtype != ZPC_FP32) return false;
   const int G = d->num_q_heads / d->num_kv_heads;
   if ((long long)G * d->window > 256) return false;
+  // kernels address a (layer, pool) plane with 32-bit element offsets: per-layer K (or V) element count
+  if ((unsigned long long)d->num_blocks * d->block_size * d->num_kv_heads * d->head_dim >= (1ull << 32)) return false;
   if (p->n_max < 2) return false;
   if (p->pool_kernel < 1 || (p->pool_kernel % 2) == 0) return false;
   if (p->max_seq_len < 1 || p->max_seq_len > ZPC_MAX_SEQ_LEN) return false;
@@ -35,6 +37,9 @@ bool desc_ok(const zpc_cache_desc* d, const zpc_params* p) {
   if (p->flags & ZPC_F_GLOBAL_SCORE) {
     if (!std::isfinite(p->global_alpha) || p->global_alpha < 0.f || p->global_alpha > 1.f) return false;
   }
+  if ((p->variant & ~ZPC_V_MASK) != 0 || ((p->variant >> ZPC_V_SELECT_SHIFT) & 3u) == 3u ||
+      ((p->variant >> ZPC_V_COMPACT_SHIFT) & 7u) > 4u)
+    return false;
   return true;
 }
 
@@ -88,6 +93,7 @@ int make_call(const zpc_cache_desc* d, const zpc_params* p, const zpc_batch* b, 
   if (b->table_stride < 1 && b->num_requests > 0) return ZPC_ERR_INVALID_ARG;
   if ((p->flags & ZPC_F_PREFIX) && !b->ref_counts) return ZPC_ERR_INVALID_ARG;
   if ((p->flags & ZPC_F_GLOBAL_SCORE) && (!b->global_scores || !b->is_compressed)) return ZPC_ERR_INVALID_ARG;
+  if ((p->flags & ZPC_F_POOL_FIRST) && b->num_requests > 0 && !b->is_compressed) return ZPC_ERR_INVALID_ARG;
   if ((p->flags & ZPC_F_LSE_INPUT) && b->num_requests > 0 && !b->window_lse) return ZPC_ERR_INVALID_ARG;
   if ((reinterpret_cast<uintptr_t>(b->workspace) & (kAlign - 1)) != 0) return ZPC_ERR_INVALID_ARG;
   if (b->workspace_bytes < ls.pub.total_bytes) return ZPC_ERR_WORKSPACE;
@@ -101,6 +107,7 @@ int make_call(const zpc_cache_desc* d, const zpc_params* p, const zpc_batch* b, 
   c->G = d->num_q_heads / d->num_kv_heads; c->d = d->head_dim; c->b = d->block_size;
   c->N_total = d->num_blocks; c->M = d->num_q_slots; c->w = d->window; c->dtype = d->dtype;
   c->n_max = p->n_max; c->pool_kernel = p->pool_kernel; c->max_seq_len = p->max_seq_len; c->flags = p->flags;
+  c->variant = p->variant;
   c->R = b->num_requests; c->table_stride = b->table_stride;
   c->free_capacity = b->free_capacity; c->freed_capacity = b->freed_capacity;
   c->k_cache = b->k_cache; c->v_cache = b->v_cache; c->q_cache = b->q_cache;
@@ -249,7 +256,7 @@ int zpc_compress_host(const zpc_cache_desc* d, const zpc_params* p, const zpc_ba
     cudaMemcpyAsync(seq_lens, h->seq_lens, (size_t)R * 4, H2D, s);
     cudaMemcpyAsync(tables, h->block_tables, (size_t)R * h->table_stride * 4, H2D, s);
     cudaMemcpyAsync(budgets, h->budgets, units * 4, H2D, s);
-    if ((p->flags & ZPC_F_GLOBAL_SCORE) && h->is_compressed)
+    if ((p->flags & (ZPC_F_GLOBAL_SCORE | ZPC_F_POOL_FIRST)) && h->is_compressed)
       cudaMemcpyAsync(comp, h->is_compressed, (size_t)R * 4, H2D, s);
   }
   if (h->ref_counts) cudaMemcpyAsync(refs, h->ref_counts, (size_t)d->num_blocks * 4, H2D, s);
@@ -290,6 +297,7 @@ const char* zpc_status_string(int code) {
     case ZPC_ERR_SEQ_TOO_LONG: return "seq_len > max_seq_len";
     case ZPC_ERR_BAD_SLOT: return "query slot out of range";
     case ZPC_ERR_CAPACITY: return "freed list or free stack capacity exceeded";
+    case ZPC_ERR_NONFINITE: return "non-finite Q or K value (ZPC_F_VALIDATE)";
     default: return "unknown";
   }
 }

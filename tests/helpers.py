@@ -90,16 +90,20 @@ def check_band(kept_gpu, s_ref_final, ell, where=""):
     assert not np.any(kept[must_drop]), f"{where}: kept a token below the band"
 
 
-def full_check(w, inp, res, pool=None, strict_select=True, blockwise=False, window_lse_in=None):
+def full_check(w, inp, res, pool=None, strict_select=True, blockwise=False, window_lse_in=None,
+               pool_first_compressed=None):
     """Every parity rule of §8(c) on a fully materialised (small) workload. window_lse_in: the
-    normalisers given to a ZPC_F_LSE_INPUT call (NEXT-4), passed to the oracle as well."""
-    geo, prm = geometry(w), oparams(w, pool=pool)
+    normalisers given to a ZPC_F_LSE_INPUT call (NEXT-4), passed to the oracle as well.
+    pool_first_compressed: the is_compressed[R] of a ZPC_F_POOL_FIRST call (R32): those requests select
+    on the unpooled score."""
+    pf = pool_first_compressed
+    geo, prm = geometry(w), oparams(w, pool=pool, flags=O.F_POOL_FIRST if pf is not None else 0)
     cfg = w.cfg
     R = len(inp["seq"])
     ref = O.compress(geo, prm, inp["k"], inp["v"], inp["q"], inp["slots"], inp["seq"], inp["tables"],
                      inp["budgets"], inp["refs"], inp["stack"], inp["top"], blockwise=blockwise,
                      free_capacity=len(inp["stack"]), freed_capacity=len(to_host(w.freed)),
-                     window_lse_in=window_lse_in)
+                     window_lse_in=window_lse_in, is_compressed=pf)
     assert res["status"] == ref.status == O.OK, (res["status"], ref.status)
     gpu_kept = {}
     for r in range(R):
@@ -114,17 +118,18 @@ def full_check(w, inp, res, pool=None, strict_select=True, blockwise=False, wind
                 assert ell == ref.new_lens[r, l, h], where
                 kg = res["kept"][u, :ell].copy()
                 gpu_kept[key] = kg
-                s_final = O.pin_window(O.max_pool(ref.scores[key], prm.pool_kernel), T, cfg.w)
+                kp = 1 if (pf is not None and pf[r]) else prm.pool_kernel
+                s_final = O.pin_window(O.max_pool(ref.scores[key], kp), T, cfg.w)
                 check_band(kg, s_final, ell, where)
                 if strict_select:
                     # GPU's own fp32 S through the oracle's pool+pin+select: must match bit for bit
                     s32 = res["S"][u, :T].astype(np.float64)
-                    sel = O.select(O.pin_window(O.max_pool(s32, prm.pool_kernel), T, cfg.w), ell)
+                    sel = O.select(O.pin_window(O.max_pool(s32, kp), T, cfg.w), ell)
                     np.testing.assert_array_equal(sel, kg, err_msg=where)
     # bytes: oracle compaction driven by the GPU's kept lists reproduces the whole pool
     ref2 = O.compress(geo, prm, inp["k"], inp["v"], inp["q"], inp["slots"], inp["seq"], inp["tables"],
                       inp["budgets"], inp["refs"], inp["stack"], inp["top"], kept_override=gpu_kept,
-                      free_capacity=len(inp["stack"]), freed_capacity=len(to_host(w.freed)))
+                      free_capacity=len(inp["stack"]), freed_capacity=len(to_host(w.freed)), is_compressed=pf)
     np.testing.assert_array_equal(res["k"], ref2.k_cache)
     np.testing.assert_array_equal(res["v"], ref2.v_cache)
     np.testing.assert_array_equal(res["tables"], ref2.fin.tables)

@@ -25,7 +25,7 @@ def test_library_exports_every_declared_symbol():
     L = zipc.lib()
     for name in header_functions():
         assert hasattr(L, name), name
-    assert zipc.zpc_abi_version() == zipc.ABI_VERSION == 3
+    assert zipc.zpc_abi_version() == zipc.ABI_VERSION == 4
 
 
 def _desc(**kw):
@@ -64,7 +64,24 @@ def test_redundancy_region_and_params():
     assert zipc.zpc_workspace_bytes(_desc(b=64, dtype="fp32"), p1, 4) == 0   # fp32: one warp per block, b <= 32
     assert zipc.zpc_workspace_bytes(_desc(b=40), p1, 4) == 0                   # bf16 tile kernel: multiples of 16
     assert zipc.zpc_workspace_bytes(_desc(b=512), p1, 4) == 0                  # ... up to 256
-    assert zipc.zpc_workspace_bytes(_desc(b=256), p1, 4) > 0                   # the paper's b = 256
+    assert zipc.zpc_workspace_bytes(_desc(b=256, N_total=2000), p1, 4) > 0     # the paper's b = 256
+
+
+def test_per_layer_offset_overflow_rejected():
+    """Kernels address a layer's K/V plane with 32-bit element offsets: a per-layer pool of >= 2^32
+    elements (N_total * b * h_kv * d) is ZPC_ERR_INVALID_ARG (workspace size 0), one block fewer is fine."""
+    p = zipc.make_params(129, 7, 8192)
+    limit = (1 << 32) // (16 * 4 * 128)   # 524288 blocks of b = 16, h_kv = 4, d = 128
+    assert zipc.zpc_workspace_bytes(_desc(N_total=limit), p, 4) == 0
+    assert zipc.zpc_workspace_bytes(_desc(N_total=limit - 1), p, 4) > 0
+
+
+def test_variant_bits_validated():
+    d = _desc()
+    assert zipc.zpc_workspace_bytes(d, zipc.make_params(129, 7, 8192, variant=zipc.variant(select=2, compact_nt=512)), 4) > 0
+    assert zipc.zpc_workspace_bytes(d, zipc.make_params(129, 7, 8192, variant=3 << zipc.ZPC_V_SELECT_SHIFT), 4) == 0
+    assert zipc.zpc_workspace_bytes(d, zipc.make_params(129, 7, 8192, variant=5 << zipc.ZPC_V_COMPACT_SHIFT), 4) == 0
+    assert zipc.zpc_workspace_bytes(d, zipc.make_params(129, 7, 8192, variant=1 << 20), 4) == 0
 
 
 @pytest.mark.parametrize("bad", [dict(h_q=30), dict(d=96), dict(w=0), dict(dtype=7), dict(h_q=4 * 9, w=32)])

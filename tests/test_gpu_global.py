@@ -25,8 +25,8 @@ pytestmark = pytest.mark.gpu
 @pytest.fixture(autouse=True, params=["select_auto", "select_reg"])
 def _select_path(request, monkeypatch):
     """Run every case through both selection kernels: k_select (what these small T get by default)
-    and the register-resident k_select_reg (ZPC_SELECT_REG=2 forces it for T <= 32K)."""
-    monkeypatch.setenv("ZPC_SELECT_REG", "2" if request.param == "select_reg" else "1")
+    and the register-resident k_select_reg (params.variant select = 2 forces it for T <= 32K)."""
+    monkeypatch.setattr(zipc, "DEFAULT_VARIANT", zipc.variant(select=2 if request.param == "select_reg" else 0))
 
 ALPHA = 0.8
 CASES = {
@@ -35,6 +35,9 @@ CASES = {
     "fp32_toy": scaled(CONFIGS["toy"], pool_kernel=3),
     "bf16_8b_mixed": scaled(CONFIGS["llama8b"], L=2, h_kv=2, h_q=8, n_max=9, seq_lens=[513, 700, 1030],
                             budget=(32, 128), wave=0),
+    # three requests sharing a 160-token prefix (10 blocks): R31, the shared blocks' F is read, not stored
+    "bf16_prefix_shared": scaled(CONFIGS["prefix"], L=2, h_kv=2, h_q=14, n_max=9, seq_lens=[400] * 3,
+                                 prefix_tokens=160, budget=128, wave=0, free_slack=4),
 }
 
 

@@ -103,15 +103,23 @@ def test_generator_device_equals_host(cuda_ok):
     np.testing.assert_array_equal(to_host(dw.q, True), hw.q_cache)
 
 
-@pytest.mark.parametrize("case", ["not_triggered", "bad_budget", "no_free", "bad_slot", "bad_table"])
+@pytest.mark.parametrize("case", ["not_triggered", "bad_budget", "no_free", "bad_slot", "bad_table", "capacity",
+                                  "nonfinite_k", "nonfinite_q"])
 def test_device_errors_mutate_nothing(cuda_ok, case):
     cfg = scaled(CONFIGS["prefix"], L=1, h_kv=2, h_q=14, n_max=9, seq_lens=[300, 300], prefix_tokens=64,
                  budget=128, wave=0, free_slack=4)
     hw = make_host_workload(cfg, 8)
     expect = {"not_triggered": zipc.ZPC_ERR_NOT_TRIGGERED, "bad_budget": zipc.ZPC_ERR_BAD_BUDGET,
               "no_free": zipc.ZPC_ERR_NO_FREE_BLOCKS, "bad_slot": zipc.ZPC_ERR_BAD_SLOT,
-              "bad_table": zipc.ZPC_ERR_BAD_TABLE}[case]
+              "bad_table": zipc.ZPC_ERR_BAD_TABLE, "capacity": zipc.ZPC_ERR_CAPACITY,
+              "nonfinite_k": zipc.ZPC_ERR_NONFINITE, "nonfinite_q": zipc.ZPC_ERR_NONFINITE}[case]
     lay = hw.layout
+    flags = zipc.ZPC_F_VALIDATE if case.startswith("nonfinite") else 0
+    if case == "nonfinite_k":   # one key element of request 1, layer 0, head 1, token 137 -> bf16 NaN
+        t = 137
+        hw.k_cache[0, lay.tables[1, t // cfg.b], t % cfg.b, 1, 5] = 0x7FC0
+    elif case == "nonfinite_q":   # a window query element of request 0 (head group of KV head 0) -> +inf
+        hw.q_cache[0, lay.q_slots[0], 3, 2, 7] = 0x7F80
     if case == "not_triggered":
         lay.seq_lens[1] = 16 * 8
     elif case == "bad_budget":
@@ -123,8 +131,11 @@ def test_device_errors_mutate_nothing(cuda_ok, case):
     elif case == "bad_table":
         lay.tables[1, 10] = lay.N_total
     w = from_host(hw)
+    if case == "capacity":   # a freed-list buffer one entry shorter than the blocks the call frees
+        need = sum(int(np.ceil(T / cfg.b)) - 1 - (cfg.n_max - 1) for T in lay.seq_lens) + 0
+        w.freed = w.freed[:need - 1].clone()
     before = snapshot_inputs(w)
-    desc, params = run_gpu(w)
+    desc, params = run_gpu(w, flags=flags)
     assert int(w.status.item()) == expect
     np.testing.assert_array_equal(to_host(w.k, True), before["k"])
     np.testing.assert_array_equal(to_host(w.tables), before["tables"])
@@ -132,10 +143,11 @@ def test_device_errors_mutate_nothing(cuda_ok, case):
     assert int(w.free_top.item()) == before["top"]
     np.testing.assert_array_equal(to_host(w.ref_counts), before["refs"])
     # oracle agrees on the code
-    ref = O.plan(O.Geometry(cfg.L, cfg.h_kv, cfg.h_q, cfg.d, cfg.b, lay.N_total, lay.M, cfg.w, cfg.dtype),
-                 O.Params(cfg.n_max, flags=O.F_PREFIX, max_seq_len=w.max_seq_len), before["seq"],
-                 before["tables"], before["budgets"], before["refs"], before["stack"], before["top"],
-                 before["slots"])
+    geo = O.Geometry(cfg.L, cfg.h_kv, cfg.h_q, cfg.d, cfg.b, lay.N_total, lay.M, cfg.w, cfg.dtype)
+    prm = O.Params(cfg.n_max, flags=O.F_PREFIX | (O.F_VALIDATE if flags else 0), max_seq_len=w.max_seq_len)
+    ref = O.compress(geo, prm, before["k"], before["v"], before["q"], before["slots"], before["seq"],
+                     before["tables"], before["budgets"], before["refs"], before["stack"], before["top"],
+                     free_capacity=len(before["stack"]), freed_capacity=int(w.freed.numel()))
     assert ref.status == expect
 
 
@@ -191,16 +203,14 @@ def test_deterministic(cuda_ok):
 
 # Several units per persistent CTA cluster (192 units > the 74 clusters of a B200), so the overlapped
 # schedule interleaves pass 1 of one unit with pass 2 of the previous one on every cluster, with ragged
-# lengths (partial last tiles, a unit whose 256-token pair tile is half empty). Each scoring kernel
-# variant is selected through its launch-time switch (ZPC_SCORE_OVL / ZPC_SCORE_PAIR, read per launch).
-@pytest.mark.parametrize("variant", ["ovl", "pair", "serial"])
+# lengths (partial last tiles, a unit whose 256-token pair tile is half empty). "default" is the cooperative
+# pair kernel for G = 5, 7, 8 and the overlapped kernel for G = 4; "serial" forces k_score_tc
+# (params.variant ZPC_V_SCORE_SERIAL).
+@pytest.mark.parametrize("variant", ["default", "serial"])
 @pytest.mark.parametrize("shape", [("qwen7b", 7), ("qwen32b", 5), ("llama8b", 4), ("llama8b", 8)])
 def test_many_units_per_cluster(cuda_ok, monkeypatch, variant, shape):
     name, G = shape
-    if variant == "pair" and G not in (7, 8):
-        pytest.skip("the CTA-pair kernel covers G*w/2 >= 112 columns per CTA (G = 7, 8)")
-    monkeypatch.setenv("ZPC_SCORE_OVL", "0" if variant == "serial" else "1")
-    monkeypatch.setenv("ZPC_SCORE_PAIR", "1" if variant == "pair" else "0")
+    monkeypatch.setattr(zipc, "DEFAULT_VARIANT", zipc.variant(score_serial=variant == "serial"))
     cfg = scaled(CONFIGS[name], L=4, h_kv=8, h_q=8 * G, n_max=9,
                  seq_lens=[300, 1100, 144, 700, 385, 896], budget=(32, 128), wave=0, free_slack=6)
     _run(cfg, seed=11 + G)
@@ -210,7 +220,7 @@ def test_many_units_per_cluster(cuda_ok, monkeypatch, variant, shape):
 # ragged units run through the 256 x 32 / 512 x 32 / 1024 x 32 variants (and k_select for comparison)
 @pytest.mark.parametrize("max_seq_len,mode", [(2048, "2"), (8192, "1"), (16384, "1"), (32768, "1"), (8192, "0")])
 def test_select_kernels(cuda_ok, monkeypatch, max_seq_len, mode):
-    monkeypatch.setenv("ZPC_SELECT_REG", mode)
+    monkeypatch.setattr(zipc, "DEFAULT_VARIANT", zipc.variant(select={"0": 1, "1": 0, "2": 2}[mode]))
     cfg = scaled(CONFIGS["qwen7b"], L=2, h_kv=4, h_q=28, n_max=9, seq_lens=[300, 1100, 144, 700, 385],
                  budget=(32, 128), wave=0, free_slack=6, pool_kernel=7)
     _run(cfg, seed=21, max_seq_len=max_seq_len)
@@ -220,7 +230,7 @@ def test_select_kernels(cuda_ok, monkeypatch, max_seq_len, mode):
 # k_p: the other widths through the register kernel too (strict selection pins the pooled keys)
 @pytest.mark.parametrize("pool", [1, 3, 5, 9])
 def test_select_reg_other_pools(cuda_ok, monkeypatch, pool):
-    monkeypatch.setenv("ZPC_SELECT_REG", "2")
+    monkeypatch.setattr(zipc, "DEFAULT_VARIANT", zipc.variant(select=2))
     cfg = scaled(CONFIGS["qwen7b"], L=1, h_kv=4, h_q=28, n_max=9, seq_lens=[300, 1100, 144, 385],
                  budget=(32, 128), wave=0, free_slack=6, pool_kernel=pool)
     _run(cfg, seed=23, pool=pool, max_seq_len=2048)
@@ -228,10 +238,25 @@ def test_select_reg_other_pools(cuda_ok, monkeypatch, pool):
 
 @pytest.mark.parametrize("nt", [128, 256, 512, 1024])
 def test_compact_every_cta_width(cuda_ok, monkeypatch, nt):
-    """k_compact at each CTA width launch_compact can pick (ZPC_COMPACT_NT overrides the per-call choice):
+    """k_compact at each CTA width launch_compact can pick (params.variant overrides the per-call choice):
     chunk = NT/VPR ranks, so the hazard ordering (reads of a chunk before its writes, kept[i] >= i) is
     exercised at 8..128 ranks per chunk, for VPR = 16 (bf16 d = 128) and VPR = 8 (bf16 d = 64)."""
-    monkeypatch.setenv("ZPC_COMPACT_NT", str(nt))
+    monkeypatch.setattr(zipc, "DEFAULT_VARIANT", zipc.variant(compact_nt=nt))
     _run(SMALL7B, seed=40 + nt)
     cfg = scaled(CONFIGS["qwen32b"], L=2, h_kv=2, h_q=10, d=64, n_max=6, seq_lens=[200, 333], budget=80, wave=0)
     _run(cfg, seed=41 + nt)
+
+
+def test_pool_first_only(cuda_ok):
+    """ZPC_F_POOL_FIRST (R32): requests compressed before select on the unpooled score,
+    first-time requests on the k_p = 7 pooled one; every parity rule with the oracle doing the same."""
+    cfg = scaled(CONFIGS["qwen7b"], L=2, h_kv=2, h_q=14, n_max=9, seq_lens=[300, 257, 416, 257], budget=128,
+                 free_slack=5, pool_kernel=7)
+    hw = make_host_workload(cfg, 13)
+    hw.is_compressed = np.array([1, 0, 1, 0], np.int32)
+    w = from_host(hw)
+    inp = snapshot_inputs(w)
+    desc, params = desc_params(w, flags=zipc.ZPC_F_POOL_FIRST)
+    zipc.zpc_compress(desc, params, batch_of(w, desc, params))
+    torch.cuda.synchronize()
+    full_check(w, inp, gpu_results(w, desc, params), pool_first_compressed=hw.is_compressed)

@@ -30,8 +30,8 @@ pytestmark = pytest.mark.gpu
 @pytest.fixture(autouse=True, params=["select_auto", "select_reg"])
 def _select_path(request, monkeypatch):
     """Run every case through both selection kernels: k_select (what these small T get by default)
-    and the register-resident k_select_reg (ZPC_SELECT_REG=2 forces it for T <= 32K)."""
-    monkeypatch.setenv("ZPC_SELECT_REG", "2" if request.param == "select_reg" else "1")
+    and the register-resident k_select_reg (params.variant select = 2 forces it for T <= 32K)."""
+    monkeypatch.setattr(zipc, "DEFAULT_VARIANT", zipc.variant(select=2 if request.param == "select_reg" else 0))
 
 LAM, TAU, P = 0.2, 0.4, 0.8
 MARGIN = 2e-5

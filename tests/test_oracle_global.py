@@ -34,6 +34,28 @@ def test_alg2_hand_example():
     np.testing.assert_array_equal(f[3, 2:, 0], [9.0, 9.0])             # slots >= T untouched
 
 
+def test_shared_prefix_blocks_are_read_not_written():
+    """R31: with n_prefix = 1 the first block (shared by several requests)
+    still contributes alpha * F to the scores but its F entries are not overwritten; the private blocks
+    are updated as in the hand example above."""
+    b, n_max, T, alpha = 4, 3, 10, 0.5
+    table = [2, 0, 3]
+    f = np.zeros((4, b, 1), np.float32)
+    f[2, :, 0] = [0.8, 0.0, 0.2, 0.3]
+    f[0, :, 0] = [0.1, 0.6, 0.0, 0.0]
+    s = np.array([0.1, 0.2, 0.3, 0.05, 0.1, 0.1, 0.1, 0.1, 0.02, 0.03])
+    out = O.global_score_update(s, f, table, T, 0, b, n_max, True, alpha, n_prefix=1)
+    np.testing.assert_allclose(out[:4], [0.4, 0.2, 0.3, 0.15])        # history still read
+    np.testing.assert_array_equal(f[2, :, 0], np.float32([0.8, 0.0, 0.2, 0.3]))   # shared: unchanged
+    np.testing.assert_allclose(f[0, :, 0], np.float32([0.1, 0.3, 0.1, 0.1]))      # private: updated
+    f2 = np.zeros((4, b, 1), np.float32)
+    out2 = O.global_score_update(s, f2, table, T, 0, b, n_max, False, alpha, n_prefix=2)
+    np.testing.assert_array_equal(out2, s)                            # never compressed: S unchanged
+    np.testing.assert_array_equal(f2[2], 0)
+    np.testing.assert_array_equal(f2[0], 0)
+    np.testing.assert_allclose(f2[3, :2, 0], np.float32(s[8:10]))
+
+
 def test_uncompressed_stores_only():
     b, T = 4, 9
     f = np.full((3, b, 2), 7.0, np.float32)
@@ -93,3 +115,19 @@ def test_dominating_history_and_relocation():
         rank = np.arange(len(kept))
         np.testing.assert_array_equal(g.f_cache[l, np.asarray(tg)[rank // cfg.b], rank % cfg.b, h],
                                       np.float32(s[kept]))
+
+
+def test_pool_first_only_pools_first_compressions():
+    """R32: with F_POOL_FIRST a request compressed before (r = 0) selects on the unpooled
+    score and a first-time request (r = 1) on the pooled one: each kept set equals the plain method's with
+    that pool width, and the two widths really select differently here."""
+    cfg, hw, geo, f0, prm, run = _setup(compressed=(1, 0))
+    pf = run(O.Params(n_max=cfg.n_max, pool_kernel=7, flags=O.F_POOL_FIRST), None)
+    pooled = run(O.Params(n_max=cfg.n_max, pool_kernel=7), None)
+    unpooled = run(O.Params(n_max=cfg.n_max, pool_kernel=1), None)
+    differ = False
+    for (r, l, h), kept in pf.kept.items():
+        ref = (unpooled if r == 0 else pooled).kept[(r, l, h)]
+        np.testing.assert_array_equal(kept, ref)
+        differ |= not np.array_equal(pooled.kept[(r, l, h)], unpooled.kept[(r, l, h)])
+    assert differ

@@ -301,6 +301,47 @@ def test_plan_errors():
     assert O.plan(geo, O.Params(n_max=4), np.array([32]), t2, bud, None, stack, 10).status == O.ERR_BAD_TABLE
 
 
+def test_plan_capacity_by_hand():
+    """R18 on the Fig. 1 structure: A has N = 5, B has N = 7 blocks, b = 4,
+    N_max = 4, no sharing -> the call frees 1 + 3 = 4 private blocks and pops none. The freed list needs
+    4 entries; the free stack, with top = 4, grows to 4 + 4 = 8. One entry less in either buffer is
+    ZPC_ERR_CAPACITY, checked before anything else is planned."""
+    geo = O.Geometry(L=1, h_kv=1, h_q=1, d=2, b=4, N_total=16, M=2, w=2, dtype="fp32")
+    prm = O.Params(n_max=4)
+    tables = np.array([[0, 1, 2, 3, 4, -1, -1], [5, 6, 7, 8, 9, 10, 11]], np.int32)
+    stack = np.zeros(16, np.int32)
+    stack[:4] = [12, 13, 14, 15]
+    seq, bud = np.array([20, 25]), np.full((2, 1, 1), 12)
+    run = lambda fc, dc: O.plan(geo, prm, seq, tables, bud, None, stack, 4, None, fc, dc).status  # noqa: E731
+    assert run(8, 4) == O.OK
+    assert run(8, 3) == O.ERR_CAPACITY          # freed list one short
+    assert run(7, 4) == O.ERR_CAPACITY          # free stack one short
+    assert run(None, None) == O.OK              # unchecked when the caller gives no capacities
+    # with a prefix: 2 shared blocks held only by this batch (ref = 2 = their occurrences) are driven to 0
+    # and freed too, so both buffers need 2 more entries; a third external reference keeps them alive
+    t2 = np.array([[0, 1, 2, 3, 4, -1, -1], [0, 1, 7, 8, 9, 10, 11]], np.int32)
+    refs = np.zeros(16, np.int32)
+    refs[t2[t2 >= 0]] = 1
+    refs[[0, 1]] = 2
+    p2 = O.Params(n_max=4, flags=O.F_PREFIX)
+    st2 = np.zeros(16, np.int32)
+    st2[:6] = [5, 6, 12, 13, 14, 15]
+    pl = O.plan(geo, p2, seq, t2, bud, refs, st2, 6, None, 100, 100)
+    assert pl.status == O.OK
+    n_fresh = sum(min(int(pl.n_prefix[r]), 3) for r in range(2)) + sum(
+        1 for r in range(2) if max(int(pl.n_prefix[r]), 3) >= [5, 7][r])
+    freed = (5 - 1 - 3) + (7 - 1 - 3) + 2      # private non-targets + the two zeroed shared blocks
+    need_stack = 6 - n_fresh + freed
+    run2 = lambda fc, dc, rf: O.plan(geo, p2, seq, t2, bud, rf, st2, 6, None, fc, dc).status  # noqa: E731
+    assert run2(need_stack, freed, refs) == O.OK
+    assert run2(need_stack, freed - 1, refs) == O.ERR_CAPACITY
+    assert run2(need_stack - 1, freed, refs) == O.ERR_CAPACITY
+    refs3 = refs.copy()
+    refs3[[0, 1]] = 3                           # held outside the batch: not freed
+    assert run2(need_stack - 2, freed - 2, refs3) == O.OK
+    assert run2(need_stack - 2, freed - 3, refs3) == O.ERR_CAPACITY
+
+
 def test_block_conservation_random():
     """No leak, no double free: new tables + freed + still-held shared +
     free stack after == old tables + free stack before, as multisets with no duplicates."""
@@ -381,3 +422,42 @@ def test_prefix_compress_structure(prefix_tokens, seq):
                 for rank, t in enumerate(kept):
                     np.testing.assert_array_equal(out.v_cache[l, tg[rank // 4], rank % 4, h],
                                                   hw.v_cache[l, lay.tables[r, t // 4], t % 4, h])
+
+
+def test_widen_known_answers():
+    """bf16 widening by bit placement (the stored 16 bits are the top half of an fp32): known values,
+    including the smallest subnormal 2^-133, signed zero, infinities and NaN; fp32 passes through."""
+    bits = np.array([0x3F80, 0xC000, 0x0001, 0x3FC0, 0x8000, 0x7F80, 0xFF80, 0x7FC0, 0x4049, 0x0080], np.uint16)
+    out = O.widen(bits, "bf16")
+    np.testing.assert_array_equal(out[:5], [1.0, -2.0, 2.0 ** -133, 1.5, 0.0])
+    assert np.signbit(out[4])
+    assert out[5] == np.inf and out[6] == -np.inf and np.isnan(out[7])
+    assert out[8] == 3.140625                          # 0x4049: 1.5703125 * 2
+    assert out[9] == 2.0 ** -126                       # smallest normal
+    f = np.array([1.5, -0.1, 3e-40], np.float32)
+    np.testing.assert_array_equal(O.widen(f, "fp32"), f.astype(np.float64))
+
+
+def test_unit_keys_gather_by_construction():
+    """unit_keys returns row t = K[l, table[t // b], t % b, h]: a pool whose element 0 encodes
+    (layer, block, slot, head) is read back through a scrambled table, and the same rows come out of
+    logits_dense (G = 1, w = 1, q = e_0 * sqrt(d)) -- the two gathers agree."""
+    L, NT, b, hk, d = 2, 9, 4, 3, 4
+    k = np.zeros((L, NT, b, hk, d))
+    for l in range(L):
+        for blk in range(NT):
+            for s in range(b):
+                for h in range(hk):
+                    k[l, blk, s, h, 0] = 10000 * l + 100 * blk + 10 * s + h
+    table = [7, 2, 5, 0]
+    T = 14
+    geo = O.Geometry(L=L, h_kv=hk, h_q=hk, d=d, b=b, N_total=NT, M=1, w=1, dtype="fp32")
+    for l in range(L):
+        for h in range(hk):
+            rows = O.unit_keys(geo, k, table, T, l, h)
+            expect = [10000 * l + 100 * table[t // b] + 10 * (t % b) + h for t in range(T)]
+            np.testing.assert_array_equal(rows[:, 0], expect)
+            q = np.zeros((1, hk, d))
+            q[0, h, 0] = np.sqrt(d)
+            lg = O.logits_dense(geo, q, k[l], table, T, h)
+            np.testing.assert_allclose(lg[0, 0], expect)
