@@ -159,11 +159,44 @@ def cpu_model():
 
 
 # ---------------------------------------------------------------- sharding (multi-GPU, weak scaling)
-def shard_rids(rank, world, per_gpu, R_total):
-    """Global request ids compressed by `rank`: a contiguous block of per_gpu ids (wrapping over
-    the config's R_total), so every rank's workload has the same shape (weak scaling) and data
-    are keyed by global request id (identical bytes whatever the GPU count)."""
+def shard_rids(rank, world, per_gpu, R_total, scaling="weak"):
+    """Global request ids compressed by `rank` (data are keyed by global request id, so a request's
+    bytes and results do not depend on the GPU count; contiguous ranges).
+    weak:   a contiguous block of per_gpu ids per rank (wrapping over the config's R_total), so every
+            rank's workload has the same shape;
+    strong: the per_gpu-request batch of one GPU split into contiguous ranges over the ranks (the
+            total work is fixed; P = 8 on qwen7b leaves 8 requests = 896 units per GPU)."""
+    if scaling == "strong":
+        lo, hi = rank * per_gpu // world, (rank + 1) * per_gpu // world
+        return np.arange(lo, hi) % R_total
     return np.arange(rank * per_gpu, (rank + 1) * per_gpu) % R_total
+
+
+CHECK_MOD = (1 << 61) - 1
+CHECK_P = 1_000_003
+
+
+def output_checksum(w, desc, params, rids):
+    """Sharding-invariant checksum of a call's selection (the kept lists determine every byte the
+    compaction moves): per unit a polynomial hash of its kept positions, weighted by the unit's GLOBAL
+    identity (request id, layer, head), summed mod 2^61-1. The sum over ranks equals a single-GPU run of
+    the same request ids."""
+    import torch
+    from paper_2603_08743_b200 import zipc
+    cfg = w.cfg
+    R = len(rids)
+    lay = zipc.zpc_workspace_layout_get(desc, params, R)
+    units = R * cfg.L * cfg.h_kv
+    ks = lay.kept_stride
+    kept = w.workspace[lay.kept:lay.kept + 4 * units * ks].view(torch.int32).view(units, ks).to(torch.int64)
+    ell = w.new_lens.reshape(units).to(torch.int64)
+    pw = torch.from_numpy(np.array([pow(CHECK_P, i, (1 << 31) - 1) for i in range(ks)], np.int64)).to(kept.device)
+    mask = torch.arange(ks, device=kept.device)[None, :] < ell[:, None]
+    hu = (((kept + 1) * pw[None, :]) * mask).sum(1) % ((1 << 31) - 1)          # per unit, < 2^31
+    gid = (torch.from_numpy(np.asarray(rids, np.int64)).to(kept.device)[:, None] * (cfg.L * cfg.h_kv)
+           + torch.arange(cfg.L * cfg.h_kv, device=kept.device)[None, :]).reshape(units) + 1
+    prod = (hu * (gid % ((1 << 29) - 3))).cpu().numpy()                         # < 2^60 each
+    return int(sum(int(x) for x in prod) % CHECK_MOD)                             # exact (Python ints)
 
 
 def max_over_ranks(value, dist=None, device=None):
@@ -256,6 +289,8 @@ def main():
                          "the normalisers a decode engine would hold are produced untimed by one two-pass "
                          "zpc_score call before the timed steps")
     ap.add_argument("--wave", type=int, default=0, help="requests per call per GPU (default: the config's)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: per_gpu requests on every rank; strong: the one-GPU batch split over the ranks")
     ap.add_argument("--graph", action="store_true",
                     help="NEXT-3: replay the whole step as one captured CUDA graph (launch-bound small batches); "
                          "value/ms_per_step then come from the graph replays, stage_ms from the eager steps")
@@ -310,7 +345,7 @@ def main():
     from paper_2603_08743_b200.batch import batch_of, desc_params, window_lse_from_two_pass
     from zpc_inputs.device import generate
 
-    rids = shard_rids(rank, world, per_gpu, cfg.R)
+    rids = shard_rids(rank, world, per_gpu, cfg.R, args.scaling)
     w = generate(cfg, args.seed, rids, device=dev)
     flags = zipc.ZPC_F_COUNT_MOVES | (zipc.ZPC_F_SCORE_CUDACORE if args.cudacore else 0)
     if args.lse_input:
@@ -406,13 +441,32 @@ def main():
         step_ms_total = g_ms
         graph_info = {"graph_ms_per_step": g_ms / args.steps, "eager_ms_per_step": eager_ms / args.steps}
     max_ms = max_over_ranks(step_ms_total, dist, dev)
-    R_all = per_gpu * world
     ms_per_step = max_ms / args.steps
-    value = R_all / (ms_per_step / 1000.0)
     T_sum = int(lay.seq_lens.sum())
-
+    checksum = output_checksum(w, desc, params, rids)
     peaks = load_peaks()
     ab = algorithmic_bytes(cfg, lay.seq_lens, w.budgets_host, moves, args.lse_input)
+    # per-rank record, all-gathered over NCCL (SURVEY.md §8(d) timing protocol): time, requests, sum T,
+    # moved rows, algorithmic bytes, output checksum
+    rec = [step_ms_total / args.steps, len(rids), T_sum, moves, ab["score"] + ab["select"] + ab["compact"],
+           checksum]
+    if world > 1:
+        t = torch.tensor(rec, dtype=torch.float64, device=dev)
+        ck = torch.tensor([checksum], dtype=torch.int64, device=dev)
+        g_rec = [torch.zeros_like(t) for _ in range(world)]
+        g_ck = [torch.zeros_like(ck) for _ in range(world)]
+        dist.all_gather(g_rec, t)
+        dist.all_gather(g_ck, ck)
+        ranks = [dict(ms_per_step=float(x[0]), requests=int(x[1]), sum_T=int(x[2]), moved_rows=int(x[3]),
+                      algorithmic_bytes=int(x[4]), checksum=int(c.item())) for x, c in zip(g_rec, g_ck)]
+    else:
+        ranks = [dict(ms_per_step=rec[0], requests=rec[1], sum_T=rec[2], moved_rows=rec[3], algorithmic_bytes=rec[4],
+                      checksum=checksum)]
+    R_all = sum(r["requests"] for r in ranks)
+    T_all = sum(r["sum_T"] for r in ranks)
+    value = R_all / (ms_per_step / 1000.0)
+    job_checksum = sum(r["checksum"] for r in ranks) % CHECK_MOD
+
     score_ms = stage_ms[stage_names.index("score")] / args.steps
     compact_ms = stage_ms[stage_names.index("compact")] / args.steps
     step_bytes = ab["score"] + ab["select"] + ab["compact"]
@@ -435,7 +489,8 @@ def main():
         **({"redundancy_roofline": redundancy_roofline(cfg, lay.seq_lens, world,
                                                         stage_ms[stage_names.index("redundancy")] / args.steps,
                                                         peaks)} if args.redundancy else {}),
-        "kv_tokens_per_s": T_sum * world / (ms_per_step / 1e3),
+        "kv_tokens_per_s": T_all / (ms_per_step / 1e3),
+        "ranks": ranks, "output_checksum": job_checksum,
         **({"cuda_graph": graph_info} if graph_info else {}),
         "wall_s_incl_restores": wall,
     }
@@ -498,12 +553,14 @@ def main():
     if rank == 0:
         line = {"metric": "requests_compressed_per_s", "value": value, "unit": "req/s", "n_gpus": world,
                 "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_per_step,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": cfg.dtype,
+                "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": cfg.dtype,
                 "data": "synthetic (zpc_inputs Philox recipe, generated in HBM)",
-                "config": {"workload": workload, "requests_per_gpu": per_gpu,
+                "config": {"workload": workload, "requests_per_gpu": per_gpu if args.scaling == "weak" else len(rids),
+                           "requests_total": R_all,
                            "l2": "pool > L2 (15 GB K for qwen7b); modified blocks restored from a pristine copy "
                                  "between steps (untimed, writes > L2)",
-                           "parallelism": f"request-sharded x{world}, no data-path collective"},
+                           "parallelism": f"request-sharded x{world} ({args.scaling} scaling), no data-path "
+                                          f"collective; NCCL all-gathers the per-rank stats"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches_per_step * args.steps, "clocks": clocks, **extra}
         print(json.dumps(line))

@@ -96,3 +96,13 @@ def test_query_slots_distinct(R):
     cfg = scaled(CONFIGS["qwen7b"], L=1, seq_lens=[300] * R)
     lay = make_layout(cfg, 0, np.arange(R))
     assert len(set(lay.q_slots.tolist())) == R and (lay.q_slots < lay.M).all()
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
+def test_strong_shards_are_contiguous_and_complete(world):
+    """--scaling strong (contiguous ranges): the 64-request qwen7b batch split over P ranks."""
+    ids = [bench.shard_rids(r, world, 64, 64, "strong") for r in range(world)]
+    flat = np.concatenate(ids)
+    assert flat.tolist() == list(range(64))
+    assert all(np.all(np.diff(x) == 1) for x in ids if len(x) > 1)
+    assert max(len(x) for x in ids) - min(len(x) for x in ids) <= 1
