@@ -210,14 +210,14 @@ def max_over_ranks(value, dist=None, device=None):
 
 
 # ---------------------------------------------------------------- measured DRAM traffic
-TRAFFIC_FILE = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_traffic.json")
+TRAFFIC_FILE = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r02_traffic.json")
 
 
 def measured_traffic(cfg, per_gpu, lse_input=False):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu --set full capture
-    of this exact workload (profiles/r01_traffic.json: the full qwen7b batch, 64 requests;
+    of this exact workload (profiles/r02_traffic.json: the full qwen7b batch, 64 requests;
     profiles/r01_traffic_lse.json: the same with --lse-input), else {}."""
-    path = TRAFFIC_FILE.replace(".json", "_lse.json") if lse_input else TRAFFIC_FILE
+    path = TRAFFIC_FILE.replace("r02_traffic.json", "r01_traffic_lse.json") if lse_input else TRAFFIC_FILE
     if cfg.name != "qwen7b" or per_gpu != 64 or not os.path.exists(path):
         return {}
     try:
@@ -227,7 +227,7 @@ def measured_traffic(cfg, per_gpu, lse_input=False):
     out = {}
     for name, rec in kern.items():
         tot = rec["dram_bytes_read"] + rec["dram_bytes_write"]
-        if any(f"{k}<{cfg.h_q // cfg.h_kv}, {cfg.w}, {cfg.d}" in name for k in ("k_score_tc", "k_score_ovl", "k_score_pair")):
+        if any(f"{k}<{cfg.h_q // cfg.h_kv}, {cfg.w}, {cfg.d}" in name for k in ("k_score_tc", "k_score_ovl", "k_score_coop")):
             out["score"] = tot
         elif "k_compact" in name:
             out["compact"] = tot
@@ -243,7 +243,7 @@ def redundancy_roofline(cfg, seq_lens, world, red_ms, peaks):
     if cfg.dtype == "bf16" and cfg.b == 16:
         kern = "k_red_mma"
     elif cfg.dtype == "bf16" and cfg.b % 16 == 0 and 16 < cfg.b <= 256:
-        kern = "k_red_tile"
+        kern = "k_red_umma"
     else:
         kern = "k_red_generic"
     # the within-block Gram matrices: b x b x d multiply-adds per block
@@ -252,6 +252,31 @@ def redundancy_roofline(cfg, seq_lens, world, red_ms, peaks):
             "achieved": ach, "peak": peaks["hbm"], "unit": "GB/s", "frac": ach / peaks["hbm"] if ach else None,
             "algorithmic_bytes_per_launch": byts, "ms": red_ms,
             "gram_tflops": flops / (red_ms / 1e3) / 1e12 if red_ms else None}
+
+
+def score_roofline(ab, passes, score_ms, peaks, traffic):
+    """Roofline of the score kernel (a1+a2), SURVEY §8(d). Its arithmetic intensity is passes x G*w flop per
+    K byte (2*G*w*d flops per token per pass over T*d*e bytes); above the measured ridge (bf16 TF/s / HBM
+    GB/s, ~254 flop/B) the kernel is tensor-bound: the default two-pass call at G*w = 224 (qwen7b) is at
+    448 flop/B. Then `achieved` is the algorithmic two-pass contraction (no M padding, no normaliser
+    K-step) in TFLOP/s against the measured bf16 peak; the north star's HBM fraction is kept beside it."""
+    secs = score_ms / 1e3
+    flops = ab["flops_score"] * passes
+    hbm_gbs = ab["score"] / secs / 1e9
+    hbm = {"achieved": hbm_gbs, "peak": peaks["hbm"], "unit": "GB/s", "frac": hbm_gbs / peaks["hbm"],
+           "algorithmic_bytes_per_launch": ab["score"]}
+    ridge = peaks["bf16"] * 1e12 / (peaks["hbm"] * 1e9)
+    intensity = flops / ab["score"]
+    base = {"kernel": "score (a1+a2)", "passes": passes, "intensity_flop_per_byte": intensity,
+            "ridge_flop_per_byte": ridge, "peak_src": peaks["src"], "traffic": traffic,
+            "traffic_unit": "bytes/launch (dram read+write, ncu --set full)"}
+    if intensity > ridge:
+        tf = flops / secs / 1e12
+        return {**base, "bound": "tensor", "achieved": tf, "peak": peaks["bf16"], "unit": "TFLOP/s",
+                "frac": tf / peaks["bf16"], "algorithmic_flops_per_launch": flops,
+                "frac_of_sustained": tf / peaks["bf16_sust"],
+                "hbm": hbm}
+    return {**base, "bound": "hbm", **hbm}
 
 
 # ---------------------------------------------------------------- GPU arm
@@ -471,13 +496,9 @@ def main():
     compact_ms = stage_ms[stage_names.index("compact")] / args.steps
     step_bytes = ab["score"] + ab["select"] + ab["compact"]
     traffic = measured_traffic(cfg, per_gpu, args.lse_input)
-    roofline = {"kernel": "score (a1+a2)", "bound": "hbm", "achieved": ab["score"] / (score_ms / 1e3) / 1e9,
-                "peak": peaks["hbm"], "unit": "GB/s", "peak_src": peaks["src"],
-                "traffic": traffic.get("score"), "traffic_unit": "bytes/launch (dram read+write, ncu --set full)",
-                "algorithmic_bytes_per_launch": ab["score"]}
-    roofline["frac"] = roofline["achieved"] / roofline["peak"]
     passes = 1 if args.lse_input else 2
     tensor_tf = ab["flops_score"] * passes / (score_ms / 1e3) / 1e12   # passes x 2*G*w*d per token
+    roofline = score_roofline(ab, passes, score_ms, peaks, traffic.get("score"))
     extra = {
         "stage_ms": {n: round(float(x) / args.steps, 4) for n, x in zip(stage_names, stage_ms)},
         "score_tensor_tflops": tensor_tf, "score_passes": passes,

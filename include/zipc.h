@@ -152,7 +152,9 @@ typedef struct {
                                           instead of the cooperative / overlapped ones */
 #define ZPC_V_SELECT_SHIFT   4         /* bits 4..5: 0 auto, 1 k_select, 2 k_select_reg (T <= 32K) */
 #define ZPC_V_COMPACT_SHIFT  8         /* bits 8..10: 0 auto, 1..4 = k_compact CTA width 128/256/512/1024 */
-#define ZPC_V_MASK           0x733u
+#define ZPC_V_RED_MMASYNC    (1u << 12) /* ZPC_F_REDUNDANCY, bf16 b = 32..256: the mma.sync block-Gram kernel
+                                          (k_red_tile) instead of the tcgen05 one (k_red_umma) */
+#define ZPC_V_MASK           0x1733u
 
 #define ZPC_MAX_SEQ_LEN 49152   /* select keeps a unit's scores in shared memory */
 

@@ -14,8 +14,21 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared", "-
           "-Xptxas", "-v"]
 
 
-def _nvcc(srcs, out, includes, extra=()):
-    cmd = [NVCC, *ARCH, *COMMON, *[f"-I{i}" for i in includes], *extra, "-o", out, *srcs]
+def _link(objs, out):
+    newest = max(os.path.getmtime(o) for o in objs)
+    if os.path.exists(out) and os.path.getmtime(out) >= newest and not os.environ.get("ZPC_REBUILD"):
+        return out
+    cmd = [NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", out, *objs]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stderr[-8000:])
+        raise RuntimeError(f"link failed for {out}")
+    return out
+
+
+def _nvcc(srcs, out, includes, extra=(), shared=True):
+    common = COMMON if shared else [c for c in COMMON if c != "-shared"]
+    cmd = [NVCC, *ARCH, *common, *[f"-I{i}" for i in includes], *extra, "-o", out, *srcs]
     newest = max(os.path.getmtime(s) for s in srcs + [os.path.join(i, f) for i in includes
                                                       for f in os.listdir(i) if f.endswith(".h")])
     if os.path.exists(out) and os.path.getmtime(out) >= newest and not os.environ.get("ZPC_REBUILD"):
@@ -32,12 +45,20 @@ def _nvcc(srcs, out, includes, extra=()):
 
 
 def build_lib():
+    """Each .cu is compiled to its own object in parallel (-c), then linked into the shared library."""
+    from concurrent.futures import ThreadPoolExecutor
     csrc = os.path.join(HERE, "csrc")
     srcs = sorted(os.path.join(csrc, f) for f in os.listdir(csrc) if f.endswith(".cu"))
     # ZPC_EXTRA_NVCC / ZPC_LIB_OUT: an alternative build of the same sources (A/B timing via ZPC_LIB)
     out = os.environ.get("ZPC_LIB_OUT") or os.path.join(HERE, "lib", "libzipc.so")
     extra = os.environ.get("ZPC_EXTRA_NVCC", "").split()
-    return _nvcc(srcs, out, [os.path.join(ROOT, "include"), csrc], extra)
+    incs = [os.path.join(ROOT, "include"), csrc]
+    objdir = os.path.join(os.path.dirname(out), "obj_" + os.path.basename(out).replace(".so", ""))
+    os.makedirs(objdir, exist_ok=True)
+    objs = [os.path.join(objdir, os.path.basename(s).replace(".cu", ".o")) for s in srcs]
+    with ThreadPoolExecutor(max_workers=len(srcs)) as ex:
+        list(ex.map(lambda so: _nvcc([so[0]], so[1], incs, [*extra, "-c"], shared=False), zip(srcs, objs)))
+    return _link(objs, out)
 
 
 def build_gen():

@@ -85,6 +85,7 @@ inline int coop_cmax(int max_seq_len) { return ((max_seq_len + 255) / 256 + kCoo
 cudaError_t launch_select(const Call& c, cudaStream_t s);
 cudaError_t launch_compact(const Call& c, cudaStream_t s);
 cudaError_t launch_redundancy(const Call& c, cudaStream_t s);
+cudaError_t launch_redundancy_tc(const Call& c, cudaStream_t s);   // k_red_umma (redundancy_tc.cu)
 
 // ---- device helpers ----
 __device__ __forceinline__ float ex2f(float x) {

@@ -426,6 +426,8 @@ cudaError_t launch_redundancy(const Call& c, cudaStream_t s) {
     const dim3 grid(units, (nb_max + kWarps * kBlocksPerWarp - 1) / (kWarps * kBlocksPerWarp));
     if (c.d == 128) k_red_mma<128><<<grid, kWarps * 32, 0, s>>>(c);
     else k_red_mma<64><<<grid, kWarps * 32, 0, s>>>(c);
+  } else if (c.dtype == ZPC_BF16 && c.b > 16 && c.b % 16 == 0 && c.b <= 256 && !(c.variant & ZPC_V_RED_MMASYNC)) {
+    return launch_redundancy_tc(c, s);
   } else if (c.dtype == ZPC_BF16 && c.b > 16 && c.b % 16 == 0 && c.b <= 256) {
     const dim3 grid(units, (c.max_seq_len + c.b - 1) / c.b);
     const size_t smem = tile_smem_bytes(c.d, c.b);

@@ -70,10 +70,17 @@ constexpr int kDescRing = 16;     // step descriptors in flight (feeder -> loade
 constexpr uint32_t kDescEnd = 0xFFFFFFFFu;
 // step descriptor: bit 0 kind (0 pass 1, 1 pass 2), bit 1 first tile of the chunk, bit 2 last tile,
 // bits 3..14 tile index k in the chunk, bits 15..30 chunk sequence number j of this pair
-__device__ __forceinline__ uint32_t desc_pack(int kind, int k, int nt, int j) {
-  return (uint32_t)kind | ((k == 0) ? 2u : 0u) | ((k + 1 == nt) ? 4u : 0u) | ((uint32_t)(k & 0xFFF) << 3) |
+// (bits 1/2 follow the step's position in the chunk's sequence; the tile index is the tile it reads)
+__device__ __forceinline__ uint32_t desc_pack(int kind, int k, int nt, int j, int tile) {
+  return (uint32_t)kind | ((k == 0) ? 2u : 0u) | ((k + 1 == nt) ? 4u : 0u) | ((uint32_t)(tile & 0xFFF) << 3) |
          ((uint32_t)(j & 0xFFFF) << 15);
 }
+#ifndef ZPC_COOP_REV
+#define ZPC_COOP_REV 0   // 1: pass 2 walks a chunk's tiles last-to-first: the tiles pass 1 read last are re-read first
+                         // (measured: no fewer DRAM bytes, 2% slower -- the re-reads miss L2 either way)
+#endif
+// tile read by the k-th pass-2 step of a chunk of nt tiles
+__device__ __forceinline__ int p2_tile(int k, int nt) { return ZPC_COOP_REV ? nt - 1 - k : k; }
 
 // ------------------------------------------------------------------ pass-1 exp sums (packed)
 template <int PE>
@@ -586,8 +593,9 @@ __global__ void __launch_bounds__(kCThreads, 1) k_score_coop(Call c, CoopArgs a,
         if (!ended && sched_next()) {
           const volatile int* ce = ctab + kCtabInts * (ls.j & 7);
           const int T = ce[0], r = ce[1], tb = ce[4], nt = ce[8];
-          dsc = desc_pack(ls.kind, ls.k, nt, ls.j);
-          const int t0 = (tb + ls.k) * 2 * kTile + rank * kTile;
+          const int tile = ls.kind == 1 ? p2_tile(ls.k, nt) : ls.k;
+          dsc = desc_pack(ls.kind, ls.k, nt, ls.j, tile);
+          const int t0 = (tb + tile) * 2 * kTile + rank * kTile;
           if (t0 < T) {
             const int j0 = t0 / c.b;
             const int nb = (min(t0 + kTile, T) - 1) / c.b - j0 + 1;
@@ -806,7 +814,7 @@ __global__ void __launch_bounds__(kCThreads, 1) k_score_coop(Call c, CoopArgs a,
         B.T = ce[0]; B.tb = ce[4]; B.nt = ce[8];
       }
       for (int k = 0; k < B.nt; ++k, ++n2) {
-        const int t = (B.tb + k) * 2 * kTile + rank * kTile + q * 32 + lane;
+        const int t = (B.tb + p2_tile(k, B.nt)) * 2 * kTile + rank * kTile + q * 32 + lane;
         const int du = t - (B.T - W);   // window row u contributes iff u >= du (token t <= T-w+u)
         float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll 1

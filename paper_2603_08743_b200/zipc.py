@@ -47,13 +47,16 @@ ZPC_MAX_SEQ_LEN = 49152
 ZPC_V_SCORE_SERIAL = 1
 ZPC_V_SELECT_SHIFT = 4
 ZPC_V_COMPACT_SHIFT = 8
+ZPC_V_RED_MMASYNC = 1 << 12
 DEFAULT_VARIANT = 0
 
 
-def variant(score_serial=False, select=0, compact_nt=0) -> int:
-    """select: 0 auto, 1 k_select, 2 k_select_reg; compact_nt: 0 auto or 128/256/512/1024."""
+def variant(score_serial=False, select=0, compact_nt=0, red_mmasync=False) -> int:
+    """select: 0 auto, 1 k_select, 2 k_select_reg; compact_nt: 0 auto or 128/256/512/1024;
+    red_mmasync: the mma.sync redundancy kernel (k_red_tile) instead of k_red_umma."""
     cw = {0: 0, 128: 1, 256: 2, 512: 3, 1024: 4}[compact_nt]
-    return (ZPC_V_SCORE_SERIAL if score_serial else 0) | (select << ZPC_V_SELECT_SHIFT) | (cw << ZPC_V_COMPACT_SHIFT)
+    return ((ZPC_V_SCORE_SERIAL if score_serial else 0) | (select << ZPC_V_SELECT_SHIFT) |
+            (cw << ZPC_V_COMPACT_SHIFT) | (ZPC_V_RED_MMASYNC if red_mmasync else 0))
 
 # exported symbols (the judge's / tests' export check compares with include/zipc.h)
 EXPORTS = ["zpc_workspace_bytes", "zpc_workspace_layout_get", "zpc_compress", "zpc_plan", "zpc_score",

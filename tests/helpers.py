@@ -90,6 +90,45 @@ def check_band(kept_gpu, s_ref_final, ell, where=""):
     assert not np.any(kept[must_drop]), f"{where}: kept a token below the band"
 
 
+def check_band_tokens(kept_gpu, s_ref_final, eps, ell, where=""):
+    """Kept-set rule with a per-token error allowance eps[t] >= |s_gpu[t] - s_ref[t]| (NEXT-1, where
+    the combined score S' = pool(S) - lambda softmax(r / tau) may cross zero, so no relative band fits).
+    With L = s_ref - eps and U = s_ref + eps: a token that fewer than ell others can possibly beat
+    (#{j != t: U_j >= L_t} < ell) must be kept; one that at least ell others surely beat
+    (#{j: L_j > U_t} >= ell) must be dropped. Returns (#must-keep, #must-drop) for coverage checks."""
+    assert len(kept_gpu) == ell, where
+    assert np.all(np.diff(kept_gpu) > 0), f"{where}: kept list not strictly ascending"
+    s = np.asarray(s_ref_final, np.float64)
+    fin = np.isfinite(s)
+    lo = np.where(fin, s - eps, s)
+    hi = np.where(fin, s + eps, s)
+    hs, ls = np.sort(hi), np.sort(lo)
+    n = len(s)
+    beat_possible = n - np.searchsorted(hs, lo, side="left") - 1   # j != t with U_j >= L_t (U_t >= L_t)
+    beat_sure = n - np.searchsorted(ls, hi, side="right")           # j with L_j > U_t
+    must_keep = beat_possible < ell
+    must_drop = beat_sure >= ell
+    kept = np.zeros(n, bool)
+    kept[kept_gpu] = True
+    assert np.all(kept[must_keep]), f"{where}: dropped a token no error allowance could push out"
+    assert not np.any(kept[must_drop]), f"{where}: kept a token at least ell others surely beat"
+    return int(must_keep.sum()), int(must_drop.sum())
+
+
+def redundancy_eps(pooled, r_ref, T, lam, tau, ambiguous=None):
+    """Per-token allowance for |S'_gpu - S'_ref|, S' = pool(S) - lambda softmax(r / tau) (NEXT-1, R22):
+    1e-3 pool(S)_t (the score tolerance; max pooling keeps it) + lambda |d softmax_t|. An error
+    dr_j <= 1e-5 |r_j| + 4e-5 / T in r (the r tolerance of the NEXT-1 tests) moves softmax_t = e^{r_t/tau} / Z
+    by at most softmax_t (e^{(dr_t + max_j dr_j) / tau} - 1). `ambiguous` marks tokens whose block has a
+    cosine within the test margin of p: there the discrete zeroing may flip, moving r_t by one cosine
+    (<= 1) / T."""
+    dr = 1e-5 * np.abs(r_ref) + 4e-5 / T
+    if ambiguous is not None:
+        dr = np.where(ambiguous, dr + 1.0 / T, dr)
+    sm = O.softmax_temperature(r_ref, tau)
+    return 1e-3 * np.abs(pooled) + lam * sm * np.expm1((dr + dr.max()) / tau) + 1e-12
+
+
 def full_check(w, inp, res, pool=None, strict_select=True, blockwise=False, window_lse_in=None,
                pool_first_compressed=None):
     """Every parity rule of §8(c) on a fully materialised (small) workload. window_lse_in: the

@@ -14,7 +14,7 @@ from paper_2603_08743_b200.batch import batch_of, desc_params, workspace_view
 from zpc_inputs import CONFIGS, budgets_for, k_rows, q_rows, v_rows
 from zpc_inputs.device import generate
 
-from helpers import check_band, check_scores
+from helpers import check_band, check_band_tokens, check_scores, redundancy_eps
 
 pytestmark = pytest.mark.gpu
 
@@ -180,11 +180,21 @@ def test_redundancy_sampled_units_vs_oracle(run7b_red, r, l, h):
     lay = zipc.zpc_workspace_layout_get(desc, params, cfg.R)
     ell = int(w.new_lens[r, l, h].item())
     kg = workspace_view(w, desc, params, "kept", torch.int32, (units, lay.kept_stride))[u, :ell].cpu().numpy()
-    band = 1e-3 * np.abs(pooled).max()
-    theta = np.sort(s_ref)[::-1][ell - 1]
-    kept = np.zeros(T, bool)
-    kept[kg] = True
-    assert np.all(kept[s_ref > theta + band]) and not np.any(kept[s_ref < theta - band])
+    # per-token band (tokens of ambiguous blocks get one cosine / T of slack in r)
+    eps = redundancy_eps(pooled, ref, T, RED[0], RED[1], ambiguous=~ok)
+    nk, nd = check_band_tokens(kg, s_ref, eps, ell, f"unit {r},{l},{h}")
+    assert nk + nd >= 0.9 * T, (nk, nd)
+    # strict: the GPU's own S and r through the oracle's combine + select, where the boundary is separated
+    sg_raw = workspace_view(w, desc, params, "scores", torch.float32, (units, w.max_seq_len))[u, :T].cpu().numpy()
+    sg = O.pin_window(O.combine_redundancy(O.max_pool(sg_raw.astype(np.float64), cfg.pool_kernel),
+                                           rr.astype(np.float64), RED[0], RED[1]), T, cfg.w)
+    vals = np.sort(sg)[::-1]
+    gap = vals[ell - 1] - vals[ell]
+    tight = 1e-6 * np.abs(pooled).max()          # the fp32 combine in k_select vs fp64 here
+    if gap > tight:
+        np.testing.assert_array_equal(O.select(sg, ell), kg)
+    else:                                         # near-tie at the boundary (max pooling makes plateaus)
+        check_band_tokens(kg, sg, np.full(T, tight), ell, f"unit {r},{l},{h} (own S')")
 
 
 # ---- NEXT-4 at full size: single-pass scoring (ZPC_F_LSE_INPUT), the bench's --lse-input launch.
