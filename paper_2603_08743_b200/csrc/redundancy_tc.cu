@@ -226,8 +226,8 @@ __global__ void __launch_bounds__(kRThreads, 3) k_red_umma(Call c) {
       upk2(acc2[0], a0, a1);
       upk2(acc2[1], a2, a3);
       // the diagonal term x_ii joined the column half holding column i
-      const int ncw_i = min(128, b - (i & ~127)) / 2;   // column split of the MMA holding column i
-      const float xd = ((i & 127) / ncw_i == chalf) ? sq[i] * ni : 0.f;
+      const int ncw_i = min(128, b - (i & ~127)) >> 1;  // column split of the MMA holding column i
+      const float xd = (((i & 127) >= ncw_i) == (chalf == 1)) ? sq[i] * ni : 0.f;
       rsum[chalf * 256 + i] = ni * (((a0 + a1) + (a2 + a3)) - xd);
       zpart[chalf * 256 + i] = zj;
       zvpart[chalf * 256 + i] = zval;
