@@ -151,6 +151,9 @@ int run_score(const Call& c, cudaStream_t s) {
     cudaError_t e = launch_score_coop(c, s, &used);
     if (e != cudaSuccess) return ZPC_ERR_CUDA;
     if (used) return ZPC_OK;
+    e = launch_score_res(c, s, &used);
+    if (e != cudaSuccess) return ZPC_ERR_CUDA;
+    if (used) return ZPC_OK;
     e = launch_score_tc(c, s, &used);
     if (e != cudaSuccess) return ZPC_ERR_CUDA;
     if (used) return ZPC_OK;
