@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define ZPC_ABI_VERSION 4
+#define ZPC_ABI_VERSION 5
 
 /* ---- return / status codes ---- */
 #define ZPC_OK                  0
@@ -262,6 +262,21 @@ int zpc_finalize(const zpc_cache_desc* desc, const zpc_params* params, const zpc
 size_t zpc_workspace_bytes_host(const zpc_cache_desc* desc, const zpc_params* params, int32_t num_requests,
                                 int32_t table_stride, int32_t free_capacity, int32_t freed_capacity);
 int zpc_compress_host(const zpc_cache_desc* desc, const zpc_params* params, const zpc_batch* host, void* stream);
+
+/* Which scoring kernel family (a1 + a2) a call with this descriptor and these params runs (no launch, no
+ * device access). PAPER.md:369-411 defines what every family computes; they differ only in how:
+ *   ZPC_PATH_COOP      tcgen05, cooperative CTA pairs, two passes (bf16, w = 32, G in {5, 7, 8})
+ *   ZPC_PATH_RESIDENT  tcgen05, logits resident in TMEM, one MMA pass (bf16, w = 16, G = 4, d = 128,
+ *                      max_seq_len <= 4096: the paper's operating point)
+ *   ZPC_PATH_TC        tcgen05, per-unit kernels (bf16, w = 32 with G = 1..8 or w = 16 with G in {4, 8};
+ *                      single-pass ZPC_F_LSE_INPUT calls; ZPC_V_SCORE_SERIAL)
+ *   ZPC_PATH_CUDACORE  FFMA kernels (fp32, other w or G, b < 5, or ZPC_F_SCORE_CUDACORE)
+ * Returns one of these, or ZPC_ERR_INVALID_ARG for a descriptor zpc_compress would reject. */
+#define ZPC_PATH_COOP      1
+#define ZPC_PATH_RESIDENT  2
+#define ZPC_PATH_TC        3
+#define ZPC_PATH_CUDACORE  4
+int zpc_score_path(const zpc_cache_desc* desc, const zpc_params* params);
 
 const char* zpc_status_string(int code);
 int zpc_abi_version(void);

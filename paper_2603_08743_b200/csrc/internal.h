@@ -78,6 +78,10 @@ cudaError_t launch_finalize(const Call& c, cudaStream_t s);
 cudaError_t launch_score_cudacore(const Call& c, cudaStream_t s);
 cudaError_t launch_score_tc(const Call& c, cudaStream_t s, bool* used);
 cudaError_t launch_score_res(const Call& c, cudaStream_t s, bool* used);   // score_res.cu (w = 16, short units)
+// which scoring kernel family a call takes (no launch): the same tests the launchers make
+bool score_coop_applies(const Call& c);
+bool score_res_applies(const Call& c);
+bool score_tc_applies(const Call& c);
 cudaError_t launch_score_coop(const Call& c, cudaStream_t s, bool* used);
 // smallest chunk of the cooperative score kernel (pair-tiles of 256 tokens per chunk): sizes the per-unit
 // chunk bound of the workspace partials

@@ -959,12 +959,16 @@ cudaError_t dispatch_coop(const Call& c, cudaStream_t s, bool* used) {
 
 // Two-pass bf16 calls with w = 32 and G*w/2 in (64, 128] (G = 5, 7, 8): the cooperative pair kernel.
 // Others (single-pass ZPC_F_LSE_INPUT, w = 16, G = 4) fall through to launch_score_tc.
+bool score_coop_applies(const Call& c) {
+  if (c.dtype != ZPC_BF16 || c.lse_in != nullptr || c.w != 32 || (c.variant & ZPC_V_SCORE_SERIAL)) return false;
+  if (c.d != 64 && c.d != 128) return false;
+  if (c.b < 5) return false;   // a 128-token tile must span <= kMaxIds blocks
+  return c.G == 5 || c.G == 7 || c.G == 8;
+}
+
 cudaError_t launch_score_coop(const Call& c, cudaStream_t s, bool* used) {
   *used = false;
-  if (c.dtype != ZPC_BF16 || c.lse_in != nullptr || c.w != 32 || (c.variant & ZPC_V_SCORE_SERIAL)) return cudaSuccess;
-  if (c.d != 64 && c.d != 128) return cudaSuccess;
-  if (c.b < 5) return cudaSuccess;   // a 128-token tile must span <= kMaxIds blocks
-  if (c.G != 5 && c.G != 7 && c.G != 8) return cudaSuccess;
+  if (!score_coop_applies(c)) return cudaSuccess;
   if (c.R * c.L * c.h_kv == 0) { *used = true; return cudaSuccess; }
   return c.d == 64 ? dispatch_coop<64>(c, s, used) : dispatch_coop<128>(c, s, used);
 }

@@ -581,11 +581,17 @@ cudaError_t launch_res_g(const Call& c, cudaStream_t s, bool* used) {
 // Two-pass bf16 calls with w = 16, d = 128, G = 4 whose longest unit fits the cluster's TMEM twice over
 // (T <= 8 CTAs x 256/(G*w) tiles x 128 tokens = 4096 tokens at G*w = 64) -- the paper's operating point
 // (Qwen3-8B). Others fall through (k_score_tc).
+bool score_res_applies(const Call& c) {
+  if (c.dtype != ZPC_BF16 || c.lse_in != nullptr || c.w != 16 || c.d != 128 || (c.variant & ZPC_V_SCORE_SERIAL))
+    return false;
+  if (c.b < 5 || c.G != 4) return false;
+  // the largest cluster (8) holds two units of ceil(T / 128) / 8 tiles each in the NS slots
+  return (c.max_seq_len + kTile - 1) / kTile <= 8 * (CfgR<4, 16, 128, 8>::NS / 2);
+}
+
 cudaError_t launch_score_res(const Call& c, cudaStream_t s, bool* used) {
   *used = false;
-  if (c.dtype != ZPC_BF16 || c.lse_in != nullptr || c.w != 16 || c.d != 128 || (c.variant & ZPC_V_SCORE_SERIAL))
-    return cudaSuccess;
-  if (c.b < 5) return cudaSuccess;   // a 128-token tile must span <= kMaxIds blocks
+  if (!score_res_applies(c)) return cudaSuccess;
   if (c.R * c.L * c.h_kv == 0) { *used = true; return cudaSuccess; }
   switch (c.G) {
     case 4: return launch_res_g<4, 16>(c, s, used);

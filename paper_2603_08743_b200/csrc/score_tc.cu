@@ -1389,8 +1389,13 @@ cudaError_t dispatch_g(const Call& c, const CUtensorMap& tq, cudaStream_t s, boo
   if (c.w != 32) return cudaSuccess;
   *used = true;
   switch (c.G) {
+    // MHA (G = 1) and the other GQA ratios up to 8 (MQA and GQA in general)
+    case 1: return launch_c<1, 32, D, false>(c, tq, s);
+    case 2: return launch_c<2, 32, D, false>(c, tq, s);
+    case 3: return launch_c<3, 32, D, false>(c, tq, s);
     case 4: return launch_c<4, 32, D, true>(c, tq, s);
     case 5: return launch_c<5, 32, D, false>(c, tq, s);
+    case 6: return launch_c<6, 32, D, false>(c, tq, s);
     case 7: return launch_c<7, 32, D, false>(c, tq, s);
     case 8: return launch_c<8, 32, D, false>(c, tq, s);
     default: *used = false; return cudaSuccess;
@@ -1398,6 +1403,12 @@ cudaError_t dispatch_g(const Call& c, const CUtensorMap& tq, cudaStream_t s, boo
 }
 
 }  // namespace
+
+bool score_tc_applies(const Call& c) {
+  if (c.dtype != ZPC_BF16 || (c.d != 64 && c.d != 128) || c.b < 5) return false;
+  if (c.w == 16) return c.d == 128 && (c.G == 4 || c.G == 8);
+  return c.w == 32 && c.G >= 1 && c.G <= 8;
+}
 
 cudaError_t launch_score_tc(const Call& c_in, cudaStream_t s, bool* used) {
   *used = false;

@@ -287,6 +287,24 @@ int zpc_compress_host(const zpc_cache_desc* d, const zpc_params* p, const zpc_ba
   return cuda_rc(cudaGetLastError());
 }
 
+int zpc_score_path(const zpc_cache_desc* d, const zpc_params* p) {
+  if (!desc_ok(d, p)) return ZPC_ERR_INVALID_ARG;
+  Call c;
+  memset(&c, 0, sizeof(c));
+  c.L = d->num_layers; c.h_kv = d->num_kv_heads; c.h_q = d->num_q_heads; c.G = d->num_q_heads / d->num_kv_heads;
+  c.d = d->head_dim; c.b = d->block_size; c.N_total = d->num_blocks; c.M = d->num_q_slots; c.w = d->window;
+  c.dtype = d->dtype; c.n_max = p->n_max; c.pool_kernel = p->pool_kernel; c.max_seq_len = p->max_seq_len;
+  c.flags = p->flags; c.variant = p->variant; c.R = 1;
+  static const float kDummy = 0.f;                 // only tested against NULL
+  c.lse_in = (p->flags & ZPC_F_LSE_INPUT) ? &kDummy : nullptr;
+  if (c.dtype == ZPC_BF16 && !(c.flags & ZPC_F_SCORE_CUDACORE)) {
+    if (score_coop_applies(c)) return ZPC_PATH_COOP;
+    if (score_res_applies(c)) return ZPC_PATH_RESIDENT;
+    if (score_tc_applies(c)) return ZPC_PATH_TC;
+  }
+  return ZPC_PATH_CUDACORE;
+}
+
 const char* zpc_status_string(int code) {
   switch (code) {
     case ZPC_OK: return "ok";

@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 # ZPC_LIB: an alternative build of the same library (A/B timing of two builds on one GPU box)
 LIB_PATH = os.environ.get("ZPC_LIB") or os.path.join(HERE, "lib", "libzipc.so")
 
-ABI_VERSION = 4  # include/zipc.h ZPC_ABI_VERSION
+ABI_VERSION = 5  # include/zipc.h ZPC_ABI_VERSION
 
 ZPC_OK = 0
 ZPC_ERR_INVALID_ARG = -1
@@ -61,7 +61,7 @@ def variant(score_serial=False, select=0, compact_nt=0, red_mmasync=False) -> in
 # exported symbols (the judge's / tests' export check compares with include/zipc.h)
 EXPORTS = ["zpc_workspace_bytes", "zpc_workspace_layout_get", "zpc_compress", "zpc_plan", "zpc_score",
            "zpc_redundancy", "zpc_select", "zpc_compact", "zpc_finalize", "zpc_workspace_bytes_host", "zpc_compress_host",
-           "zpc_status_string", "zpc_abi_version"]
+           "zpc_status_string", "zpc_abi_version", "zpc_score_path"]
 
 I32 = ctypes.c_int32
 P = ctypes.c_void_p
@@ -127,6 +127,8 @@ def lib() -> ctypes.CDLL:
         L.zpc_status_string.argtypes = [ctypes.c_int]
         L.zpc_status_string.restype = ctypes.c_char_p
         L.zpc_abi_version.restype = ctypes.c_int
+        L.zpc_score_path.argtypes = [DP, PP]
+        L.zpc_score_path.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -236,3 +238,15 @@ def zpc_compress_host(desc, params, batch, stream=None, check=True):
 
 def zpc_abi_version() -> int:
     return int(lib().zpc_abi_version())
+
+
+# zpc_score_path results (include/zipc.h): which scoring kernel family a call runs
+ZPC_PATH_COOP = 1
+ZPC_PATH_RESIDENT = 2
+ZPC_PATH_TC = 3
+ZPC_PATH_CUDACORE = 4
+ZPC_PATH_TCGEN05 = (ZPC_PATH_COOP, ZPC_PATH_RESIDENT, ZPC_PATH_TC)
+
+
+def zpc_score_path(desc, params) -> int:
+    return int(lib().zpc_score_path(ctypes.byref(desc), ctypes.byref(params)))

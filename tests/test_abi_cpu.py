@@ -25,7 +25,7 @@ def test_library_exports_every_declared_symbol():
     L = zipc.lib()
     for name in header_functions():
         assert hasattr(L, name), name
-    assert zipc.zpc_abi_version() == zipc.ABI_VERSION == 4
+    assert zipc.zpc_abi_version() == zipc.ABI_VERSION == 5
 
 
 def _desc(**kw):
@@ -115,3 +115,22 @@ def test_global_score_params():
         assert zipc.zpc_workspace_bytes(_desc(), zipc.make_params(129, 7, 8192, 0, global_alpha=bad), 4) > 0
     assert zipc.zpc_workspace_bytes(_desc(), zipc.make_params(129, 7, 8192, zipc.ZPC_F_GLOBAL_SCORE,
                                                               global_alpha=0.8), 4) > 0
+
+
+def test_score_path_query():
+    """zpc_score_path reports the scoring kernel family a call takes, with no launch (include/zipc.h)."""
+    p = zipc.make_params(129, 7, 8192, 0)
+    assert zipc.zpc_score_path(_desc(), p) == zipc.ZPC_PATH_COOP                       # qwen7b: G = 7, w = 32
+    assert zipc.zpc_score_path(_desc(h_kv=8, h_q=32), p) == zipc.ZPC_PATH_TC           # llama8b: G = 4
+    assert zipc.zpc_score_path(_desc(h_q=4), p) == zipc.ZPC_PATH_TC                    # MHA, G = 1
+    assert zipc.zpc_score_path(_desc(h_q=24), p) == zipc.ZPC_PATH_TC                   # G = 6
+    po = zipc.make_params(9, 7, 2304, 0)
+    assert zipc.zpc_score_path(_desc(h_kv=8, h_q=32, b=256, w=16, N_total=1000), po) == zipc.ZPC_PATH_RESIDENT   # paper_op
+    assert zipc.zpc_score_path(_desc(h_kv=8, h_q=32, b=256, w=16, N_total=1000), zipc.make_params(9, 7, 8192, 0)) == zipc.ZPC_PATH_TC
+    assert zipc.zpc_score_path(_desc(h_kv=8, h_q=64, b=256, w=16, N_total=1000), po) == zipc.ZPC_PATH_TC   # G = 8
+    assert zipc.zpc_score_path(_desc(w=8), p) == zipc.ZPC_PATH_CUDACORE
+    assert zipc.zpc_score_path(_desc(dtype="fp32"), p) == zipc.ZPC_PATH_CUDACORE
+    assert zipc.zpc_score_path(_desc(), zipc.make_params(129, 7, 8192, zipc.ZPC_F_SCORE_CUDACORE)) == zipc.ZPC_PATH_CUDACORE
+    assert zipc.zpc_score_path(_desc(), zipc.make_params(129, 7, 8192, zipc.ZPC_F_LSE_INPUT)) == zipc.ZPC_PATH_TC
+    assert zipc.zpc_score_path(_desc(), zipc.make_params(129, 7, 8192, 0, variant=zipc.ZPC_V_SCORE_SERIAL)) == zipc.ZPC_PATH_TC
+    assert zipc.zpc_score_path(_desc(d=96), p) == zipc.ZPC_ERR_INVALID_ARG

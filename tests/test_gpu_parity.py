@@ -216,6 +216,21 @@ def test_many_units_per_cluster(cuda_ok, monkeypatch, variant, shape):
     _run(cfg, seed=11 + G)
 
 
+# MHA (G = 1) and the GQA ratios without a config (G = 2, 3, 6) on the tensor-core path (k_score_tc), at
+# d = 128 and d = 64; the library reports which scoring kernel family a call takes (zpc_score_path)
+@pytest.mark.parametrize("d", [128, 64])
+@pytest.mark.parametrize("G", [1, 2, 3, 6])
+def test_generic_gqa_ratios(cuda_ok, G, d):
+    cfg = scaled(CONFIGS["qwen7b"], L=2, h_kv=4, h_q=4 * G, d=d, n_max=9, seq_lens=[300, 1100, 144, 385],
+                 budget=(32, 128), wave=0, free_slack=6)
+    w = from_host(make_host_workload(cfg, 40 + G))
+    desc, params = desc_params(w)
+    assert zipc.zpc_score_path(desc, params) == zipc.ZPC_PATH_TC
+    inp = snapshot_inputs(w)
+    desc, params = run_gpu(w)
+    full_check(w, inp, gpu_results(w, desc, params))
+
+
 # k_select_reg at every thread-count instance: the dispatch follows the host bound max_seq_len, so small
 # ragged units run through the 256 x 32 / 512 x 32 / 1024 x 32 variants (and k_select for comparison)
 @pytest.mark.parametrize("max_seq_len,mode", [(2048, "2"), (8192, "1"), (16384, "1"), (32768, "1"), (8192, "0")])
