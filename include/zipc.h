@@ -156,7 +156,9 @@ typedef struct {
                                           (k_red_tile) instead of the tcgen05 one (k_red_umma) */
 #define ZPC_V_MASK           0x1733u
 
-#define ZPC_MAX_SEQ_LEN 49152   /* select keeps a unit's scores in shared memory */
+#define ZPC_MAX_SEQ_LEN 262144  /* units up to 48K tokens select from shared memory, longer ones from a
+                                   workspace key region (max_seq_len x 4 bytes per unit, sized by the
+                                   workspace queries) */
 
 /* Everything one call touches. Pointers are device memory. Layouts:
  *   q_slots      int32 [R]                 query slot of each request

@@ -29,6 +29,7 @@ struct Ws {
   int32_t* coop_cnt;       // [units][2]
   int32_t* coop_rs;        // [units + 2]
   int32_t coop_cmax;       // chunks per unit the part array holds
+  uint32_t* select_keys;   // [units][max_seq_len] orderable keys of k_select<true> (max_seq_len > kSelectSmemMaxT)
   int32_t kept_stride;
 };
 
@@ -86,6 +87,7 @@ cudaError_t launch_score_coop(const Call& c, cudaStream_t s, bool* used);
 // smallest chunk of the cooperative score kernel (pair-tiles of 256 tokens per chunk): sizes the per-unit
 // chunk bound of the workspace partials
 constexpr int kCoopChunkTiles = 4;
+constexpr int kSelectSmemMaxT = 49152;   // k_select keeps up to this many keys in shared memory
 inline int coop_cmax(int max_seq_len) { return ((max_seq_len + 255) / 256 + kCoopChunkTiles - 1) / kCoopChunkTiles; }
 cudaError_t launch_select(const Call& c, cudaStream_t s);
 cudaError_t launch_compact(const Call& c, cudaStream_t s);

@@ -72,9 +72,13 @@ __device__ float block_sum(float v, float* sm) {
   return x;
 }
 
+// GK = false: the unit's keys live in shared memory (T <= kSelectSmemMaxT); GK = true (longer units, up to
+// ZPC_MAX_SEQ_LEN): in the workspace region select_keys [units][max_seq_len] (L2-resident while the CTA works
+// on it); every step is the same code on the other array.
+template <bool GK>
 __global__ void __launch_bounds__(kThreads) k_select(Call c) {
   if (*c.status != ZPC_OK) return;
-  extern __shared__ uint32_t keys[];            // [T]
+  extern __shared__ uint32_t keys_smem[];       // [T] (GK = false)
   __shared__ int hist[256];
   __shared__ int sm[kWarps];
   __shared__ float fsm[kWarps];
@@ -82,6 +86,7 @@ __global__ void __launch_bounds__(kThreads) k_select(Call c) {
   __shared__ int s_need;
 
   const int unit = blockIdx.x;
+  uint32_t* keys = GK ? c.ws.select_keys + (size_t)unit * c.max_seq_len : keys_smem;
   const int h = unit % c.h_kv;
   const int l = (unit / c.h_kv) % c.L;
   const int r = unit / (c.h_kv * c.L);
@@ -468,9 +473,13 @@ cudaError_t launch_select(const Call& c, cudaStream_t s) {
     if (T <= 32 * 512) return launch(k_select_reg<512, 32>, 512);
     return launch(k_select_reg<1024, 32>, 1024);
   }
+  if (c.max_seq_len > kSelectSmemMaxT) {   // keys in the workspace (select_keys region)
+    k_select<true><<<units, kThreads, 0, s>>>(c);
+    return cudaGetLastError();
+  }
   const size_t smem = sizeof(uint32_t) * (size_t)c.max_seq_len;
-  cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_select<<<units, kThreads, smem, s>>>(c);
+  cudaFuncSetAttribute(k_select<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_select<false><<<units, kThreads, smem, s>>>(c);
   return cudaGetLastError();
 }
 

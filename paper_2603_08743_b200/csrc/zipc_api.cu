@@ -45,7 +45,7 @@ bool desc_ok(const zpc_cache_desc* d, const zpc_params* p) {
 
 struct LayoutSizes {
   zpc_workspace_layout pub;
-  size_t req_err, n_blocks, fresh_off, priv_off, glob, marks, coop_part, coop_cnt, coop_rs;
+  size_t req_err, n_blocks, fresh_off, priv_off, glob, marks, coop_part, coop_cnt, coop_rs, select_keys;
   int32_t coop_cmax;
 };
 
@@ -76,6 +76,7 @@ bool compute_layout(const zpc_cache_desc* d, const zpc_params* p, int32_t R, Lay
   o->coop_part = take(units * o->coop_cmax * G * d->window * sizeof(float));
   o->coop_cnt = take(units * 2 * sizeof(int32_t));
   o->coop_rs = take((units + 2) * sizeof(int32_t));
+  o->select_keys = take(p->max_seq_len > kSelectSmemMaxT ? units * p->max_seq_len * sizeof(uint32_t) : 0);
   o->pub.total_bytes = off;
   o->pub.kept_stride = kept_stride;
   return true;
@@ -139,6 +140,7 @@ int make_call(const zpc_cache_desc* d, const zpc_params* p, const zpc_batch* b, 
   c->ws.coop_cnt = reinterpret_cast<int32_t*>(w + ls.coop_cnt);
   c->ws.coop_rs = reinterpret_cast<int32_t*>(w + ls.coop_rs);
   c->ws.coop_cmax = ls.coop_cmax;
+  c->ws.select_keys = reinterpret_cast<uint32_t*>(w + ls.select_keys);
   c->ws.kept_stride = ls.pub.kept_stride;
   return ZPC_OK;
 }

@@ -40,7 +40,7 @@ ZPC_F_GLOBAL_SCORE = 32
 ZPC_F_LSE_INPUT = 64
 ZPC_F_POOL_FIRST = 128
 
-ZPC_MAX_SEQ_LEN = 49152
+ZPC_MAX_SEQ_LEN = 262144
 
 # zpc_params.variant (include/zipc.h ZPC_V_*): kernel-variant overrides for tests and A/B timing; every
 # variant computes the same result. DEFAULT_VARIANT is what make_params uses when none is given.

@@ -89,7 +89,7 @@ def test_invalid_descriptors(bad):
     assert zipc.zpc_workspace_bytes(_desc(**bad), zipc.make_params(129, 7, 8192), 4) == 0
 
 
-@pytest.mark.parametrize("pk,nmax,msl", [(2, 129, 8192), (7, 1, 8192), (7, 129, 0), (7, 129, 60000)])
+@pytest.mark.parametrize("pk,nmax,msl", [(2, 129, 8192), (7, 1, 8192), (7, 129, 0), (7, 129, 262145)])
 def test_invalid_params(pk, nmax, msl):
     assert zipc.zpc_workspace_bytes(_desc(), zipc.make_params(nmax, pk, msl), 4) == 0
 

@@ -231,6 +231,22 @@ def test_generic_gqa_ratios(cuda_ok, G, d):
     full_check(w, inp, gpu_results(w, desc, params))
 
 
+# Long units (the first compression after a long prefill sees T far above N_max * b): 64K and
+# 128K tokens with ragged lengths, past the 48K shared-memory select (k_select keys in the workspace), through
+# the cooperative scoring kernel and the per-unit one
+@pytest.mark.parametrize("variant", ["default", "serial"])
+@pytest.mark.parametrize("seqs", [[65536 + 77, 50001], [131072 - 5, 70001]])
+def test_long_units(cuda_ok, monkeypatch, variant, seqs):
+    monkeypatch.setattr(zipc, "DEFAULT_VARIANT", zipc.variant(score_serial=variant == "serial"))
+    cfg = scaled(CONFIGS["qwen7b"], L=1, h_kv=1, h_q=7, n_max=9, seq_lens=seqs, budget=(32, 128), wave=0,
+                 free_slack=4)
+    w = from_host(make_host_workload(cfg, 77))
+    assert w.max_seq_len > 49152
+    inp = snapshot_inputs(w)
+    desc, params = run_gpu(w)
+    full_check(w, inp, gpu_results(w, desc, params))
+
+
 # k_select_reg at every thread-count instance: the dispatch follows the host bound max_seq_len, so small
 # ragged units run through the 256 x 32 / 512 x 32 / 1024 x 32 variants (and k_select for comparison)
 @pytest.mark.parametrize("max_seq_len,mode", [(2048, "2"), (8192, "1"), (16384, "1"), (32768, "1"), (8192, "0")])
