@@ -122,25 +122,38 @@ struct CoopArgs {
                    // cp.async faults with an illegal instruction on this toolchain: measured, not used.)
   float* part;     // [units][cmax][G*w] partial log2-sum-exp of each chunk (log2 domain, scaled logits)
   int* cnt;        // [units][2] chunks of the unit published, per CTA rank (column half)
-  int* rs;         // [units + 2] first unit of each round; rs[nr] = units; rs[units + 1] = nr
+  int* rs;         // [units + 2] first work index of each round; rs[nr] = units; rs[units + 1] = nr
+  int lh_major;    // work order: 0 unit order (request-major); 1 (layer, head)-major, requests inner (shared
+                   // prefix calls: the same (l, h) of many requests run at once, so their common prefix tiles
+                   // are read from DRAM about once and from L2 by the others -- the prefix dedup)
 };
+
+// work index v -> unit (r*L + l)*h_kv + h
+__device__ __forceinline__ int coop_unit(const Call& c, const CoopArgs& a, int v) {
+  if (!a.lh_major) return v;
+  const int lh = v / c.R, r = v - lh * c.R;
+  return r * c.L * c.h_kv + lh;   // lh = l*h_kv + h
+}
 
 struct Chunk { int unit, ci, c, tb, nt, T, r, l, h, slot; };
 
 // slot p of round rho -> chunk (false: the slot is empty in this round)
 __device__ __forceinline__ bool coop_chunk(const Call& c, const CoopArgs& a, int rho, int p, Chunk& o) {
   const int HU = c.L * c.h_kv;
-  int u = a.rs[rho], off = 0;
-  const int u1 = a.rs[rho + 1];
-  while (u < u1) {
-    const int r = u / HU;
+  int v = a.rs[rho], off = 0;
+  const int v1 = a.rs[rho + 1];
+  while (v < v1) {
+    const int unit0 = coop_unit(c, a, v);
+    const int r = unit0 / HU;
     const int T = c.seq_lens[r];
     const int npt = (T + 255) >> 8;
     const int cr = (npt + a.kt - 1) / a.kt;
-    const int nu = min(u1, (r + 1) * HU) - u;
+    // a run of consecutive work items with the same chunk count: all of request r's units (unit order), or
+    // one item ((l, h)-major order: consecutive items are different requests)
+    const int nu = a.lh_major ? 1 : min(v1, (r + 1) * HU) - v;
     if (p < off + nu * cr) {
       const int q = p - off;
-      o.unit = u + q / cr;
+      o.unit = coop_unit(c, a, v + q / cr);
       o.ci = q % cr;
       o.c = cr;
       o.T = T;
@@ -153,7 +166,7 @@ __device__ __forceinline__ bool coop_chunk(const Call& c, const CoopArgs& a, int
       return true;
     }
     off += nu * cr;
-    u += nu;
+    v += nu;
   }
   return false;
 }
@@ -252,12 +265,15 @@ __global__ void __launch_bounds__(1024) k_coop_plan(Call c, CoopArgs a) {
   if (threadIdx.x == 0) {
     int rho = 0, used = 0;
     a.rs[0] = 0;
-    for (int r = 0; r < c.R; ++r) {
+    // runs of work items with one chunk count: per request (unit order) or per item ((l, h)-major)
+    const int nruns = a.lh_major ? units : c.R;
+    for (int run = 0; run < nruns; ++run) {
+      const int r = a.lh_major ? run % c.R : run;
       const int T = c.seq_lens[r];
       const int npt = (T + 255) >> 8;
       const int cr = max((npt + a.kt - 1) / a.kt, 1);
       if (cr > a.npairs) { *c.status = ZPC_ERR_SEQ_TOO_LONG; return; }   // host sized kt from max_seq_len
-      int u = r * HU, m = HU;
+      int u = a.lh_major ? run : r * HU, m = a.lh_major ? 1 : HU;
       while (m > 0) {
         const int fit = (a.npairs - used) / cr;
         if (fit == 0) { a.rs[++rho] = u; used = 0; continue; }
@@ -932,6 +948,14 @@ cudaError_t launch_coop_t(const Call& c, cudaStream_t s) {
     cudaMemsetAsync(g_trace, 0, 49152 * 4, s);
     ca.trace = g_trace;
   }
+#endif
+  // (l, h)-major order for shared-prefix calls measured SLOWER on the prefix config (score 25.7 -> 30.5 ms,
+  // L2 hit 21%): ~24 pairs reading the same prefix lines at the same moment concentrate on a few L2 slices.
+  // Kept as a tuning switch; the dedup that pays needs the prefix tiles multiplied once against all the
+  // sharing requests' queries.
+  ca.lh_major = 0;
+#ifdef ZPC_TUNING
+  if (const char* e = getenv("ZPC_COOP_LHMAJOR")) ca.lh_major = atoi(e);
 #endif
   ca.cmax = c.ws.coop_cmax;
   ca.npairs = npairs;
