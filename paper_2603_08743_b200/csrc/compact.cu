@@ -49,6 +49,7 @@ __device__ __forceinline__ void load_chunk(const Call& c, Chunk<VPR, kVec>& ch, 
         sblk = table[t / c.b]; sslot = t % c.b;
         dblk = tg[i / c.b];    dslot = i % c.b;
       }
+      ZPC_CHECK(t >= i && sblk >= 0 && sblk < c.N_total && dblk >= 0 && dblk < c.N_total);
       // vector index relative to the (layer, head) plane: (blk*b + slot)*h_kv*VPR + e
       const uint32_t src = ((uint32_t)sblk * c.b + sslot) * rowv + e;
       const uint32_t d = ((uint32_t)dblk * c.b + dslot) * rowv + e;

@@ -4,6 +4,23 @@
 #include <stdint.h>
 #include "zipc.h"
 
+// Checked builds (-DZPC_CHECKS, scripts/checked_suite.sh): device-side bounds assertions on every gathered /
+// scattered pool row, kept index and output position, failing loudly (__trap) -- the stand-in for
+// compute-sanitizer memcheck, which this pool does not offer. Compiled out of the product library.
+#ifdef ZPC_CHECKS
+#include <cstdio>
+#define ZPC_CHECK(cond)                                                                                 \
+  do {                                                                                                  \
+    if (!(cond)) {                                                                                      \
+      printf("zpc check failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__, blockIdx.x, \
+             threadIdx.x);                                                                              \
+      __trap();                                                                                         \
+    }                                                                                                   \
+  } while (0)
+#else
+#define ZPC_CHECK(cond) do { } while (0)
+#endif
+
 namespace zpc {
 
 // Resolved workspace pointers for one call (device addresses).

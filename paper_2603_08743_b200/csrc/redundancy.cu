@@ -71,6 +71,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_red_mma(Call c) {
   int4 pre[NV];
   auto fetch = [&](int jb) {                        // this lane's share of block jb's 16 rows
     const int blk = table[jb];
+    ZPC_CHECK(blk >= 0 && blk < c.N_total);
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
       const int q = lane + 32 * v, row = q / CPR, ch = q % CPR;
@@ -158,6 +159,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_red_generic(Call c) {
     const int j0 = jb * b;
     const int nvalid = min(b, T - j0);
     const int blk = table[jb];
+    ZPC_CHECK(blk >= 0 && blk < c.N_total);
     const bool mine = lane < nvalid;
     auto elem = [&](int row, int e) -> float {
       const size_t off = kv_row(c, l, blk, row, h) + e;
@@ -226,6 +228,7 @@ __global__ void __launch_bounds__(kTileThreads) k_red_tile(Call c) {
   const int j0 = jb * b;
   const int nvalid = min(b, T - j0);
   const int blk = c.tables[(size_t)r * c.table_stride + jb];
+  ZPC_CHECK(blk >= 0 && blk < c.N_total);
   const uint16_t* K = reinterpret_cast<const uint16_t*>(c.k_cache);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 

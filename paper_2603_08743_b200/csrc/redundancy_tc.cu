@@ -80,6 +80,7 @@ __global__ void __launch_bounds__(kRThreads, 3) k_red_umma(Call c) {
     constexpr int RPP = kRThreads / CPR;            // rows per pass (16 or 32)
     static_assert(RPP % 8 == 0, "swizzle phase must repeat every pass");
     const int blk = c.tables[(size_t)r * c.table_stride + jb];
+    ZPC_CHECK(blk >= 0 && blk < c.N_total);
     const int ch = tid % CPR, row0 = tid / CPR;
     const size_t hD = (size_t)c.h_kv * D;
     const uint16_t* src = reinterpret_cast<const uint16_t*>(c.k_cache) + kv_row(c, l, blk, 0, h) + ch * 8 +

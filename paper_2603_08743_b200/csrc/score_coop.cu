@@ -511,7 +511,10 @@ __global__ void __launch_bounds__(kCThreads, 1) k_score_coop(Call c, CoopArgs a,
           const uint32_t rbase = (uint32_t)rsub * hD;
           int blk[NBLK];
 #pragma unroll
-          for (int jb = 0; jb < NBLK; ++jb) blk[jb] = lds_s32(sid + 4u * (uint32_t)jb);
+          for (int jb = 0; jb < NBLK; ++jb) {
+            blk[jb] = lds_s32(sid + 4u * (uint32_t)jb);
+            ZPC_CHECK(t0 + jb * 16 >= T || (blk[jb] >= 0 && blk[jb] < c.N_total));
+          }
           if (t0 + kTile <= T) {
 #pragma unroll
             for (int jb = 0; jb < NBLK; ++jb) {
@@ -537,6 +540,7 @@ __global__ void __launch_bounds__(kCThreads, 1) k_score_coop(Call c, CoopArgs a,
             const int t = t0 + RPP * kq + rsub;
             const int jr = b_pow2 ? (t >> b_log2) : t / c.b;
             const int blk = lds_s32(sid + 4u * (uint32_t)min(max(jr - j0, 0), kMaxIds - 1));
+            ZPC_CHECK(t >= T || (blk >= 0 && blk < c.N_total && t - jr * c.b < c.b));
             off[kq] = ((uint32_t)blk * (uint32_t)c.b + (uint32_t)(t - jr * c.b)) * hD;
           }
 #pragma unroll

@@ -238,6 +238,7 @@ __global__ void __launch_bounds__(kRThreads, 1) k_score_res(Call c, const __grid
             const int t = t0 + RPP * k + rsub;
             const int jr = b_pow2 ? (t >> b_log2) : t / c.b;
             const int blk = lds_s32(sid + 4u * (uint32_t)min(max(jr - j0, 0), kMaxIds - 1));
+            ZPC_CHECK(t >= u.T || (blk >= 0 && blk < c.N_total && t - jr * c.b < c.b));
             off[k] = ((uint32_t)blk * (uint32_t)c.b + (uint32_t)(t - jr * c.b)) * hD;
           }
 #pragma unroll

@@ -315,7 +315,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
         const uint32_t rbase = (uint32_t)rsub * hD;
         int blk[NBLK];
 #pragma unroll
-        for (int jb = 0; jb < NBLK; ++jb) blk[jb] = lds_s32(sid + 4u * (uint32_t)jb);
+        for (int jb = 0; jb < NBLK; ++jb) {
+          blk[jb] = lds_s32(sid + 4u * (uint32_t)jb);
+          ZPC_CHECK(t0 + jb * 16 >= T || (blk[jb] >= 0 && blk[jb] < c.N_total));
+        }
         if (t0 + kTile <= T) {                               // full tile: no predicates
 #pragma unroll
           for (int jb = 0; jb < NBLK; ++jb) {
@@ -341,6 +344,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
           const int t = t0 + RPP * k + rsub;
           const int jr = b_pow2 ? (t >> b_log2) : t / c.b;
           const int blk = lds_s32(sid + 4u * (uint32_t)min(max(jr - j0, 0), kMaxIds - 1));
+          ZPC_CHECK(t >= T || (blk >= 0 && blk < c.N_total && t - jr * c.b < c.b));
           off[k] = ((uint32_t)blk * (uint32_t)c.b + (uint32_t)(t - jr * c.b)) * hD;
         }
         if (!(c.debug & 256u)) {
@@ -918,7 +922,10 @@ __global__ void __launch_bounds__(kThreadsO, 1) k_score_ovl(Call c, const __grid
           const uint32_t rbase = (uint32_t)rsub * hD;
           int blk[NBLK];
 #pragma unroll
-          for (int jb = 0; jb < NBLK; ++jb) blk[jb] = lds_s32(sid + 4u * (uint32_t)jb);
+          for (int jb = 0; jb < NBLK; ++jb) {
+            blk[jb] = lds_s32(sid + 4u * (uint32_t)jb);
+            ZPC_CHECK(t0 + jb * 16 >= T || (blk[jb] >= 0 && blk[jb] < c.N_total));
+          }
           if (t0 + kTile <= T) {
 #pragma unroll
             for (int jb = 0; jb < NBLK; ++jb) {
@@ -944,7 +951,8 @@ __global__ void __launch_bounds__(kThreadsO, 1) k_score_ovl(Call c, const __grid
             const int t = t0 + RPP * k + rsub;
             const int jr = b_pow2 ? (t >> b_log2) : t / c.b;
             const int blk = lds_s32(sid + 4u * (uint32_t)min(max(jr - j0, 0), kMaxIds - 1));
-            off[k] = ((uint32_t)blk * (uint32_t)c.b + (uint32_t)(t - jr * c.b)) * hD;
+            ZPC_CHECK(t >= T || (blk >= 0 && blk < c.N_total && t - jr * c.b < c.b));
+          off[k] = ((uint32_t)blk * (uint32_t)c.b + (uint32_t)(t - jr * c.b)) * hD;
           }
 #pragma unroll
           for (int k = 0; k < kTile / RPP; ++k)

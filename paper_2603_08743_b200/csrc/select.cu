@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(kThreads) k_select(Call c) {
   int32_t* out = c.ws.kept + (size_t)unit * c.ws.kept_stride;
   int o = out0;
   for (int t = t0; t < t1; ++t)
-    if (keys[t]) out[o++] = t;
+    if (keys[t]) { ZPC_CHECK(o < ell && t < T); out[o++] = t; }
 }
 
 
@@ -445,7 +445,7 @@ __global__ void __launch_bounds__(NT) k_select_reg(Call c) {
   int o = out0;
 #pragma unroll
   for (int i = 0; i < CH; ++i)
-    if (keepm >> i & 1u) out[o++] = t0 + i;
+    if (keepm >> i & 1u) { ZPC_CHECK(o < ell && t0 + i < T); out[o++] = t0 + i; }
 }
 
 }  // namespace

@@ -19,6 +19,9 @@ from zpc_inputs.device import generate  # noqa: E402
 
 nreq = int(sys.argv[1]) if len(sys.argv) > 1 else 4
 cfg = CONFIGS["paper_op"]
+if len(sys.argv) > 2:   # another sequence length (slice-placement experiments)
+    from zpc_inputs import scaled
+    cfg = scaled(cfg, seq_lens=[int(sys.argv[2])] * 64)
 w = generate(cfg, 2603, np.arange(nreq))
 desc, params = desc_params(w)
 b = batch_of(w, desc, params)
@@ -30,7 +33,7 @@ R = nreq
 lay = zipc.zpc_workspace_layout_get(desc, params, R)
 kept = workspace_view(w, desc, params, "kept", torch.int32, (R * cfg.L * cfg.h_kv, lay.kept_stride))
 tt = kept.contiguous().view(torch.int64).reshape(-1).cpu().numpy()
-C = 8
+C = int(sys.argv[3]) if len(sys.argv) > 3 else 6
 base = None
 for rk in range(C):
     t = tt[rk * 8192:(rk + 1) * 8192]
