@@ -18,12 +18,13 @@
 // multiplied into the free slots while the epilogue sweeps the current one.
 //
 // Warp roles (512 threads): 0 Q producer (TMA, double buffer), 1 MMA issuer, 3 feeder (block ids, stage
-// release), 4-7 K gather (16-B cp.async into the SW128 K-major stage), 8-15 epilogue (lane quarter q = warp & 3
-// = 32 tokens of a tile, column half hh: window rows [hh*w/2, (hh+1)*w/2)).
+// release), 4-11 epilogue (two groups of one warp per lane quarter q = warp & 3, i.e. 32 tokens of a tile),
+// 12-15 K gather (16-B cp.async into the SW128 K-major stage; highest warp ids, which the issue arbiter favours).
 #include <cuda.h>
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <type_traits>
 
 #include "internal.h"
@@ -34,7 +35,9 @@ namespace {
 
 constexpr int kRThreads = 512;
 constexpr int kRLoadWarps = 4;
-constexpr int kREpi0 = 8;
+constexpr int kREpi0 = 4;     // epilogue warps 4..11; K gather warps 12..15 (the warp arbiter favours
+                              // high warp ids: the gather must not starve behind the epilogue's sweeps)
+constexpr int kRLoad0 = 12;
 constexpr int kREpiWarps = 8;
 constexpr int kRProdRegs = 72;
 constexpr int kREpiRegs = 184;
@@ -131,7 +134,8 @@ __device__ __forceinline__ int reduced_col(int lane, int k) {
 #endif
 
 template <int G, int W, int D, int C>
-__global__ void __launch_bounds__(kRThreads, 1) k_score_res(Call c, const __grid_constant__ CUtensorMap tmap_q) {
+__global__ void __launch_bounds__(kRThreads, 1) k_score_res(Call c, const __grid_constant__ CUtensorMap tmap_q,
+                                                           const __grid_constant__ CUtensorMap tmap_k, int ktma) {
   using K = CfgR<G, W, D, C>;
   if (*c.status != ZPC_OK) return;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -154,13 +158,15 @@ __global__ void __launch_bounds__(kRThreads, 1) k_score_res(Call c, const __grid
   const int units = c.R * c.L * c.h_kv;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < K::ST; ++s) { mbar_init(full0 + 8 * s, kRLoadWarps * 32); mbar_init(empty0 + 8 * s, 1); }
+    // full: the gather threads' cp.async arrivals, or (ktma) the feeder's one expect_tx arrival + TMA bytes
+    for (int s = 0; s < K::ST; ++s) { mbar_init(full0 + 8 * s, ktma ? 1 : kRLoadWarps * 32); mbar_init(empty0 + 8 * s, 1); }
     for (int s = 0; s < K::NS; ++s) { mbar_init(sfull0 + 8 * s, 1); mbar_init(sempty0 + 8 * s, kREpiWarps / 2); }
     for (int b = 0; b < 2; ++b) { mbar_init(qfull0 + 8 * b, 1); mbar_init(qempty0 + 8 * b, 1); }
     for (int b = 0; b < 4; ++b) mbar_init(xchg0 + 8 * b, 1);   // [group][unit parity]: expect_tx + C senders' bytes
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0 && lane == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_q)));
+  if (warp == 3 && lane == 0 && ktma) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_k)));
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "r"(kTmemCols));
@@ -188,7 +194,7 @@ __global__ void __launch_bounds__(kRThreads, 1) k_score_res(Call c, const __grid
     return u;
   };
 
-  if (warp < kREpi0) {
+  if (warp < kREpi0 || warp >= kRLoad0) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRProdRegs));
     if (warp == 0) {
       // ================= Q producer: the unit's G heads x w rows, one TMA box per 64-element slab
@@ -206,13 +212,13 @@ __global__ void __launch_bounds__(kRThreads, 1) k_score_res(Call c, const __grid
         }
       }
       __syncwarp();
-    } else if (warp >= 4 && warp < 4 + kRLoadWarps) {
+    } else if (warp >= kRLoad0 && !ktma) {
       // ================= K gather: this CTA's tiles of every unit, in order (rows through the block table;
       // ids from the feeder; 16-B cp.async straight into the SW128 K-major stage)
       constexpr int CPR = D / 8;
       constexpr int RPP = kRLoadWarps * 32 / CPR;
       static_assert(RPP % 8 == 0, "the per-thread SW128 swizzle term needs rows-per-pass % 8 == 0");
-      const int et = threadIdx.x - 4 * 32;
+      const int et = threadIdx.x - kRLoad0 * 32;
       const int cr = et % CPR, rsub = et / CPR;
       const uint32_t chunk_off = (uint32_t)(cr >> 3) * K::SLAB_K;
       const uint16_t* Kg = reinterpret_cast<const uint16_t*>(c.k_cache);
@@ -273,6 +279,9 @@ __global__ void __launch_bounds__(kRThreads, 1) k_score_res(Call c, const __grid
       };
       int total = 0;
       for (int unit = cluster_id; unit < units; unit += nclusters) total += unit_info(unit).nt;
+      int p_unit = cluster_id, p_i = 0;          // TMA path: the tile being issued
+      UnitInfo p_u = l_u;
+      const uint64_t keep = policy_evict_first();
 #pragma unroll 1
       for (int k = 0; k < kIdAhead; ++k) issue_ids(k);
       for (int g = 0; g < total; ++g) {
@@ -282,7 +291,31 @@ __global__ void __launch_bounds__(kRThreads, 1) k_score_res(Call c, const __grid
           __syncwarp();
         }
         asm volatile("cp.async.wait_group %0;" ::"n"(kIdAhead) : "memory");
-        named_bar(6, kRLoadWarps * 32 + 32);
+        if (ktma) {
+          // b % 128 == 0: the tile is 128 consecutive slots of one block, one head: SLABS boxes of 64 elements
+          // x 128 rows (row stride h_kv*d) land in the SW128 K-major stage (no per-row gather instructions)
+          __syncwarp();
+          if (lane == 0) {
+            while (p_unit < units && p_i >= p_u.nt) {
+              p_unit += nclusters;
+              p_i = 0;
+              if (p_unit < units) p_u = unit_info(p_unit);
+            }
+            const int st = g % K::ST;
+            const int t0 = (p_u.tb + p_i) * kTile;
+            const int blk = lds_s32(ids_base + (uint32_t)((g % kIdSlots) * kMaxIds) * 4u);
+            ZPC_CHECK(blk >= 0 && blk < c.N_total);
+            const int row = (p_u.l * c.N_total + blk) * c.b + (t0 % c.b);
+            const uint32_t dst = smem_u32(Ks + st * K::STAGE_BYTES);
+            mbar_expect_tx(full0 + 8 * st, K::STAGE_BYTES);
+            for (int sl = 0; sl < K::SLABS; ++sl)
+              tma_load_3d(dst + sl * K::SLAB_K, &tmap_k, sl * 64, p_u.h, row, full0 + 8 * st, keep);
+            ++p_i;
+          }
+          __syncwarp();
+        } else {
+          named_bar(6, kRLoadWarps * 32 + 32);
+        }
       }
       asm volatile("cp.async.wait_all;" ::: "memory");
     } else if (warp == 1) {
@@ -515,8 +548,21 @@ cudaError_t launch_res(const Call& c, cudaStream_t s) {
           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
+  // K as [rows = L*N_total*b][h_kv][d]: one box = 128 consecutive slots x 64 elements of one head (SW128)
+  CUtensorMap tk;
+  memset(&tk, 0, sizeof(tk));
+  int ktma = 0;
+  if (c.b % kTile == 0) {
+    const cuuint64_t kdim[3] = {(cuuint64_t)c.d, (cuuint64_t)c.h_kv, (cuuint64_t)c.L * c.N_total * c.b};
+    const cuuint64_t kstr[2] = {(cuuint64_t)c.d * 2, (cuuint64_t)c.h_kv * c.d * 2};
+    const cuuint32_t kbox[3] = {64, 1, (cuuint32_t)kTile};
+    ktma = enc(&tk, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, c.k_cache, kdim, kstr, kbox, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+           CUDA_SUCCESS;
+  }
   Call cc = c;
 #ifdef ZPC_TUNING
+  if (const char* e = getenv("ZPC_RES_NOTMA")) if (atoi(e)) ktma = 0;
   if (const char* e = getenv("ZPC_SCORE_DEBUG")) cc.debug = (uint32_t)strtoul(e, nullptr, 10);
 #endif
   auto kern = k_score_res<G, W, D, C>;
@@ -543,7 +589,7 @@ cudaError_t launch_res(const Call& c, cudaStream_t s) {
   if (cudaOccupancyMaxActiveClusters(&qn, kern, &cfg) == cudaSuccess && qn > 0) max_clusters = std::min(max_clusters, qn);
   cudaGetLastError();
   cfg.gridDim = dim3((unsigned)(std::min(units, max_clusters) * C));
-  return cudaLaunchKernelEx(&cfg, kern, cc, tq);
+  return cudaLaunchKernelEx(&cfg, kern, cc, tq, tk, ktma);
 }
 
 template <int G, int W>
