@@ -16,6 +16,7 @@
 // belongs to that other row and is subtracted from its sum afterwards, in ascending column order
 // (deterministic).
 #include <algorithm>
+#include <cstring>
 
 #include "internal.h"
 #include "tc_util.h"
@@ -38,11 +39,11 @@ __host__ __device__ inline uint32_t red_tmem_cols(int b) { return b <= 32 ? 32u 
 inline size_t red_smem_bytes(int D, int b) {
   // operand rows + inv_norm, sq (zc, zv later), 2 x (row sum, last column, value) + bar, slot: <= 73.8 KB, so
   // three CTAs fit an SM
-  return (size_t)red_rows(b) * D * 2 + (size_t)256 * 4 * 8 + 64;
+  return (size_t)red_rows(b) * D * 2 + (size_t)256 * 4 * 8 + 64;   // (2 barriers + TMEM slot in the last 64 B)
 }
 
 template <int D>
-__global__ void __launch_bounds__(kRThreads, 3) k_red_umma(Call c) {
+__global__ void __launch_bounds__(kRThreads, 3) k_red_umma(Call c, const __grid_constant__ CUtensorMap tmap_k, int ktma) {
   using C = RedCfg<D>;
   if (*c.status != ZPC_OK) return;
   const int unit = blockIdx.x;
@@ -67,20 +68,32 @@ __global__ void __launch_bounds__(kRThreads, 3) k_red_umma(Call c) {
   int* zc = reinterpret_cast<int*>(inv_norm);      // [256] per column i: the row whose entry (row, i) is zeroed
   float* zv = sq;                                   //        and that entry's value (both after the epilogues)
   uint64_t* bar = reinterpret_cast<uint64_t*>(zvpart + 512);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 1);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 2);   // bar[0] MMA, bar[1] TMA load
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t base = smem_u32(smem);
   const uint32_t ncols = red_tmem_cols(b);
 
-  // ---- stage rows [0, rows) by 16-B cp.async into SW128 K-major slabs; rows >= nvalid are zero (R20).
-  // Thread t copies 16-B chunk t % CPR of rows t / CPR + k * RPP: constant source / destination strides, and
-  // the swizzle term is fixed because RPP is a multiple of 8.
-  {
+  const int blk = c.tables[(size_t)r * c.table_stride + jb];
+  ZPC_CHECK(blk >= 0 && blk < c.N_total);
+  const uint32_t lbar = smem_u32(bar + 1);         // TMA load barrier (ktma)
+  if (ktma) {
+    // the block's b rows of head h: one TMA box of b slots x 64 elements per slab (row stride h_kv*d), landing in
+    // the SW128 K-major layout; slots >= T are zeroed after it lands (R20)
+    if (tid == 0) {
+      mbar_init(lbar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      mbar_expect_tx(lbar, (uint32_t)(b * D * 2));
+      for (int sl = 0; sl < C::SLABS; ++sl)
+        tma_load_3d(base + (uint32_t)sl * slab_bytes, &tmap_k, sl * 64, h, (l * c.N_total + blk) * b, lbar,
+                    policy_evict_first());
+    }
+  } else {
+    // ---- stage rows [0, rows) by 16-B cp.async into SW128 K-major slabs; rows >= nvalid are zero (R20).
+    // Thread t copies 16-B chunk t % CPR of rows t / CPR + k * RPP: constant source / destination strides, and
+    // the swizzle term is fixed because RPP is a multiple of 8.
     constexpr int CPR = D / 8;                      // 16-B chunks per row
     constexpr int RPP = kRThreads / CPR;            // rows per pass (16 or 32)
     static_assert(RPP % 8 == 0, "swizzle phase must repeat every pass");
-    const int blk = c.tables[(size_t)r * c.table_stride + jb];
-    ZPC_CHECK(blk >= 0 && blk < c.N_total);
     const int ch = tid % CPR, row0 = tid / CPR;
     const size_t hD = (size_t)c.h_kv * D;
     const uint16_t* src = reinterpret_cast<const uint16_t*>(c.k_cache) + kv_row(c, l, blk, 0, h) + ch * 8 +
@@ -103,7 +116,19 @@ __global__ void __launch_bounds__(kRThreads, 3) k_red_umma(Call c) {
     mbar_init(smem_u32(bar), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  asm volatile("cp.async.wait_all;" ::: "memory");
+  if (ktma) {
+    __syncthreads();                                // lbar initialised before anyone waits on it
+    mbar_wait(lbar, 0);
+    if (nvalid < b) {                               // slots >= T of a partial last block: zero rows (R20)
+      for (int q = tid; q < (b - nvalid) * (D / 8); q += kRThreads) {
+        const int row = nvalid + q / (D / 8), ch = q % (D / 8);
+        *reinterpret_cast<uint4*>(smem + (ch >> 3) * slab_bytes + row * 128 + (((ch & 7) ^ (row & 7)) << 4)) =
+            make_uint4(0u, 0u, 0u, 0u);
+      }
+    }
+  } else {
+    asm volatile("cp.async.wait_all;" ::: "memory");
+  }
   __syncthreads();
   // |k_i|^2 and 1/|k_i| in fp32 (0 for a zero-norm key or an empty slot, R23)
   if (tid < b) {
@@ -275,7 +300,20 @@ cudaError_t launch_t(const Call& c, cudaStream_t s) {
   cudaError_t e = cudaFuncSetAttribute(k_red_umma<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const dim3 grid(units, (c.max_seq_len + c.b - 1) / c.b);
-  k_red_umma<D><<<grid, kRThreads, smem, s>>>(c);
+  // K as [rows = L*N_total*b][h_kv][d]; one box = a block's b slots x 64 elements of one head (SW128)
+  CUtensorMap tk;
+  memset(&tk, 0, sizeof(tk));
+  int ktma = 0;
+  if (EncodeTiledFn enc = encode_fn()) {
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const cuuint64_t kdim[3] = {(cuuint64_t)D, (cuuint64_t)c.h_kv, (cuuint64_t)c.L * c.N_total * c.b};
+    const cuuint64_t kstr[2] = {(cuuint64_t)D * 2, (cuuint64_t)c.h_kv * D * 2};
+    const cuuint32_t kbox[3] = {64, 1, (cuuint32_t)c.b};
+    ktma = enc(&tk, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, c.k_cache, kdim, kstr, kbox, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+           CUDA_SUCCESS;
+  }
+  k_red_umma<D><<<grid, kRThreads, smem, s>>>(c, tk, ktma);
   return cudaGetLastError();
 }
 
