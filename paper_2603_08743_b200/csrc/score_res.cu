@@ -55,7 +55,7 @@ struct CfgR {
   static constexpr uint32_t SLAB_K = kTile * 128;
   static constexpr uint32_t STAGE_BYTES = kTile * D * 2;
   // floats: per epilogue group red[4][GW], mloc[GW], L2[GW]; xbuf[2 groups][2 parities][C ranks][GW] float2
-  static constexpr uint32_t F_FLOATS = 12 * GW + 2 * 2 * C * GW * 2;
+  static constexpr uint32_t F_FLOATS = 12 * GW + 2 * 2 * C * GW * 2 + 8 * GW + 4;   // + wref[2][4][GW], oflag[2]
   static constexpr uint32_t MISC = F_FLOATS * 4 + kIdSlots * kMaxIds * 4 + 64 * 8;
   static constexpr int STAGES_FIT = (int)((227 * 1024 - 2 * Q_BYTES - MISC) / STAGE_BYTES);
   static constexpr int ST = STAGES_FIT > 6 ? 6 : STAGES_FIT;
@@ -159,10 +159,13 @@ __global__ void __launch_bounds__(kRThreads, 1) k_score_res(Call c, const __grid
 
   if (threadIdx.x == 0) {
     // full: the gather threads' cp.async arrivals, or (ktma) the feeder's one expect_tx arrival + TMA bytes
-    for (int s = 0; s < K::ST; ++s) { mbar_init(full0 + 8 * s, ktma ? 1 : kRLoadWarps * 32); mbar_init(empty0 + 8 * s, 1); }
+    const int fcount = ktma ? 1 : kRLoadWarps * 32;
+    for (int s = 0; s < K::ST; ++s) { mbar_init(full0 + 8 * s, fcount); mbar_init(empty0 + 8 * s, 1); }
     for (int s = 0; s < K::NS; ++s) { mbar_init(sfull0 + 8 * s, 1); mbar_init(sempty0 + 8 * s, kREpiWarps / 2); }
     for (int b = 0; b < 2; ++b) { mbar_init(qfull0 + 8 * b, 1); mbar_init(qempty0 + 8 * b, 1); }
     for (int b = 0; b < 4; ++b) mbar_init(xchg0 + 8 * b, 1);   // [group][unit parity]: expect_tx + C senders' bytes
+    int* of = reinterpret_cast<int*>(smem + K::OFF_F) + 12 * K::GW + 2 * 2 * C * K::GW * 2 + 8 * K::GW;
+    of[0] = of[1] = -1;                                          // epilogue overflow flags (unit-tagged)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0 && lane == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_q)));
@@ -357,6 +360,8 @@ __global__ void __launch_bounds__(kRThreads, 1) k_score_res(Call c, const __grid
     const int q = warp & 3, grp = ew >> 2;
     float* fb = reinterpret_cast<float*>(smem + K::OFF_F);
     float* red = fb + grp * 6 * GW;          // [4][GW] cross-quarter reduction
+    float* wref = fb + 12 * GW + 2 * 2 * C * GW * 2 + grp * 4 * GW;   // [4][GW] per-warp references
+    volatile int* oflag = reinterpret_cast<volatile int*>(fb + 12 * GW + 2 * 2 * C * GW * 2 + 8 * GW);   // [2]
     float* mloc = red + 4 * GW;              // [GW] CTA-local column max (log2 domain; reference of sweep B)
     float* L2s = mloc + GW;                  // [GW] merged log2 normaliser
     // xbuf[grp][k & 1][C][GW] (max, sum) pairs of the group's k-th unit, PUSHED by every rank of the cluster with
@@ -423,42 +428,30 @@ __global__ void __launch_bounds__(kRThreads, 1) k_score_res(Call c, const __grid
       if (tr) RTRACE(4096 + 8 * it + 0, gtimer());
       auto need_mask = [&](int i) { return (u.tb + i) * kTile + kTile - 1 > u.T - W; };   // warp-uniform
       const int tq = q * 32 + lane;
-      // ---- sweep A: per-column max over this CTA's tokens (raw logits)
       float acc[GW];
+      float mpub[GW / 128 + 1];                 // this thread's columns: published max (log2 domain)
+      float spub[GW / 128 + 1];                 //                         published sum
+      // ---- common case, ONE sweep: per-column sum of 2^(x*s - ref_q) with ref_q = the logit of the warp's first
+      //      token in the slice (lane 0, tile 0), so the sum is >= 1 and no max sweep is needed; the four
+      //      quarters' (ref, sum) pairs are merged like the cluster's. A logit ~100 log2 units above ref_q
+      //      (the sum leaves fp32 range) sends the whole unit to the exact two-sweep path below.
+      float* wr = wref + q * GW;                // this warp's references (log2 domain; 0 for an all-masked column)
 #pragma unroll
-      for (int j = 0; j < GW; ++j) acc[j] = -INFINITY;
+      for (int j = 0; j < GW; ++j) acc[j] = 0.f;
       sweep(u, kt, true, false, [&](int i, auto hc, float* v) {
         constexpr int h = decltype(hc)::value;
         if (need_mask(i)) mask32(v, h, (u.tb + i) * kTile + tq, u.T);
+        if (i == 0) {
+          if (lane == 0) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) acc[h * 32 + j] = fmaxf(acc[h * 32 + j], v[j]);
-      });
-      warp_col_reduce<GW, true>(acc, lane);
-#pragma unroll
-      for (int k = 0; k < GW / 32; ++k) red[q * GW + reduced_col<GW>(lane, k)] = acc[k];
-      named_bar(bid, 128);
-      float mpub[GW / 128 + 1];                 // this thread's columns: published max (log2 domain)
-#pragma unroll
-      for (int k = 0; k * 128 < GW; ++k) {
-        const int col = q * 32 + lane + k * 128;
-        if (col < GW) {
-          const float m = fmaxf(fmaxf(red[col], red[GW + col]), fmaxf(red[2 * GW + col], red[3 * GW + col]));
-          mloc[col] = m > -INFINITY ? m * scale : 0.f;        // all masked here -> any finite reference
-          mpub[k] = m > -INFINITY ? m * scale : -INFINITY;
+            for (int j = 0; j < 32; ++j) wr[h * 32 + j] = v[j] > -INFINITY ? v[j] * scale : 0.f;
+          }
+          __syncwarp();
         }
-      }
-      named_bar(bid, 128);
-      if (tr) RTRACE(4096 + 8 * it + 1, gtimer());
-      // ---- sweep B: per-column sum of 2^(x*s - m) over this CTA's tokens
-#pragma unroll
-      for (int j = 0; j < GW; ++j) acc[j] = 0.f;
-      const float2* mr2 = reinterpret_cast<const float2*>(mloc);   // (broadcast loads)
-      sweep(u, kt, false, false, [&](int i, auto hc, float* v) {
-        constexpr int h = decltype(hc)::value;
-        if (need_mask(i)) mask32(v, h, (u.tb + i) * kTile + tq, u.T);
+        const float2* r2 = reinterpret_cast<const float2*>(wr + h * 32);   // (broadcast loads)
 #pragma unroll
         for (int j = 0; j < 32; j += 2) {
-          const float2 m2 = mr2[(h * 32 + j) / 2];
+          const float2 m2 = r2[j / 2];
           const uint64_t a2 = fma2(pk2(v[j], v[j + 1]), pk2(scale, scale), pk2(-m2.x, -m2.y));
           float a0, a1;
           upk2(a2, a0, a1);
@@ -466,20 +459,92 @@ __global__ void __launch_bounds__(kRThreads, 1) k_score_res(Call c, const __grid
           acc[h * 32 + j + 1] += ex2f(a1);
         }
       });
+      bool ovf = false;
+#pragma unroll
+      for (int j = 0; j < GW; ++j) ovf |= !(acc[j] < 0x1p100f);
+      if (__any_sync(0xffffffffu, ovf) && lane == 0) oflag[grp] = it + 1;   // unit-tagged: no reset needed
       warp_col_reduce<GW, false>(acc, lane);
 #pragma unroll
       for (int k = 0; k < GW / 32; ++k) red[q * GW + reduced_col<GW>(lane, k)] = acc[k];
       named_bar(bid, 128);
+      if (tr) RTRACE(4096 + 8 * it + 1, gtimer());
+      if (oflag[grp] != it + 1) {
+#pragma unroll
+        for (int k = 0; k * 128 < GW; ++k) {
+          const int col = q * 32 + lane + k * 128;
+          if (col < GW) {
+            float M = -INFINITY;
+#pragma unroll
+            for (int qq = 0; qq < 4; ++qq)
+              if (red[qq * GW + col] > 0.f) M = fmaxf(M, wref[qq * GW + col]);
+            float S = 0.f;
+#pragma unroll
+            for (int qq = 0; qq < 4; ++qq)
+              if (red[qq * GW + col] > 0.f) S += red[qq * GW + col] * ex2f(wref[qq * GW + col] - M);
+            mpub[k] = M;
+            spub[k] = S;
+          }
+        }
+      } else {
+        // ---- exact path: sweep A (per-column max over this CTA's tokens), then sweep B against it
+        named_bar(bid, 128);                    // everyone has read red before it is rewritten
+#pragma unroll
+        for (int j = 0; j < GW; ++j) acc[j] = -INFINITY;
+        sweep(u, kt, false, false, [&](int i, auto hc, float* v) {
+          constexpr int h = decltype(hc)::value;
+          if (need_mask(i)) mask32(v, h, (u.tb + i) * kTile + tq, u.T);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) acc[h * 32 + j] = fmaxf(acc[h * 32 + j], v[j]);
+        });
+        warp_col_reduce<GW, true>(acc, lane);
+#pragma unroll
+        for (int k = 0; k < GW / 32; ++k) red[q * GW + reduced_col<GW>(lane, k)] = acc[k];
+        named_bar(bid, 128);
+#pragma unroll
+        for (int k = 0; k * 128 < GW; ++k) {
+          const int col = q * 32 + lane + k * 128;
+          if (col < GW) {
+            const float m = fmaxf(fmaxf(red[col], red[GW + col]), fmaxf(red[2 * GW + col], red[3 * GW + col]));
+            mloc[col] = m > -INFINITY ? m * scale : 0.f;        // all masked here -> any finite reference
+            mpub[k] = m > -INFINITY ? m * scale : -INFINITY;
+          }
+        }
+        named_bar(bid, 128);
+#pragma unroll
+        for (int j = 0; j < GW; ++j) acc[j] = 0.f;
+        const float2* mr2 = reinterpret_cast<const float2*>(mloc);   // (broadcast loads)
+        sweep(u, kt, false, false, [&](int i, auto hc, float* v) {
+          constexpr int h = decltype(hc)::value;
+          if (need_mask(i)) mask32(v, h, (u.tb + i) * kTile + tq, u.T);
+#pragma unroll
+          for (int j = 0; j < 32; j += 2) {
+            const float2 m2 = mr2[(h * 32 + j) / 2];
+            const uint64_t a2 = fma2(pk2(v[j], v[j + 1]), pk2(scale, scale), pk2(-m2.x, -m2.y));
+            float a0, a1;
+            upk2(a2, a0, a1);
+            acc[h * 32 + j] += ex2f(a0);
+            acc[h * 32 + j + 1] += ex2f(a1);
+          }
+        });
+        warp_col_reduce<GW, false>(acc, lane);
+#pragma unroll
+        for (int k = 0; k < GW / 32; ++k) red[q * GW + reduced_col<GW>(lane, k)] = acc[k];
+        named_bar(bid, 128);
+#pragma unroll
+        for (int k = 0; k * 128 < GW; ++k) {
+          const int col = q * 32 + lane + k * 128;
+          if (col < GW) spub[k] = (red[col] + red[GW + col]) + (red[2 * GW + col] + red[3 * GW + col]);
+        }
+      }
       // ---- exchange: each column's (max, sum) pushed to slot [rank][col] of every rank's xbuf
       if (tr) RTRACE(4096 + 8 * it + 2, gtimer());
 #pragma unroll
       for (int k = 0; k * 128 < GW; ++k) {
         const int col = q * 32 + lane + k * 128;
         if (col < GW) {
-          const float sm = (red[col] + red[GW + col]) + (red[2 * GW + col] + red[3 * GW + col]);
           const uint32_t la = smem_u32(xb + rank * GW + col);
 #pragma unroll
-          for (int rr = 0; rr < C; ++rr) st_async_v2(la, xbar, rr, mpub[k], sm);
+          for (int rr = 0; rr < C; ++rr) st_async_v2(la, xbar, rr, mpub[k], spub[k]);
         }
       }
       mbar_wait(xbar, (it >> 2) & 1);            // every rank's pairs landed (complete_tx)
@@ -556,13 +621,14 @@ cudaError_t launch_res(const Call& c, cudaStream_t s) {
     const cuuint64_t kdim[3] = {(cuuint64_t)c.d, (cuuint64_t)c.h_kv, (cuuint64_t)c.L * c.N_total * c.b};
     const cuuint64_t kstr[2] = {(cuuint64_t)c.d * 2, (cuuint64_t)c.h_kv * c.d * 2};
     const cuuint32_t kbox[3] = {64, 1, (cuuint32_t)kTile};
-    ktma = enc(&tk, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, c.k_cache, kdim, kstr, kbox, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
-           CUDA_SUCCESS;
+    if (enc(&tk, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, c.k_cache, kdim, kstr, kbox, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+        CUDA_SUCCESS)
+      ktma = 1;   // (a TMA slab 0 + cp.async slab 1 split measured no faster: 0.187 vs 0.184 ms)
   }
   Call cc = c;
 #ifdef ZPC_TUNING
-  if (const char* e = getenv("ZPC_RES_NOTMA")) if (atoi(e)) ktma = 0;
+  if (const char* e = getenv("ZPC_RES_KTMA")) ktma = std::min(ktma, atoi(e));   // A/B: 0 cp.async, 1 TMA
   if (const char* e = getenv("ZPC_SCORE_DEBUG")) cc.debug = (uint32_t)strtoul(e, nullptr, 10);
 #endif
   auto kern = k_score_res<G, W, D, C>;
