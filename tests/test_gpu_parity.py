@@ -82,6 +82,25 @@ def test_paper_operating_point_shape(cuda_ok, flags):
     _run(cfg, seed=8, flags=flags)
 
 
+def test_paper_op_normaliser_overflow_path(cuda_ok):
+    """k_score_res's one-sweep normaliser uses the logit of each warp's first token as the exp2 reference; a
+    logit ~100 log2 units above it must send the unit to the exact max-then-sum path. Key rows scaled by 2^6
+    (exact in bf16) make such logits; the oracle (fp64, max-subtracted softmax) must still be matched."""
+    cfg = scaled(CONFIGS["paper_op"], L=1, h_kv=2, h_q=8, seq_lens=[2304, 2100], wave=0, free_slack=3)
+    hw = make_host_workload(cfg, 5)
+    lay = hw.layout
+    for t in (700, 1500):                                  # inside slices, never a warp's first token
+        blk, slot = lay.tables[0, t // cfg.b], t % cfg.b
+        row = hw.k_cache[0, blk, slot, 0].astype(np.uint32) << 16
+        f = (row.view(np.float32) * 64.0).astype(np.float32)
+        hw.k_cache[0, blk, slot, 0] = (f.view(np.uint32) >> 16).astype(np.uint16)
+    w = from_host(hw)
+    inp = snapshot_inputs(w)
+    desc, params = run_gpu(w)
+    assert zipc.zpc_score_path(desc, params) == zipc.ZPC_PATH_RESIDENT
+    full_check(w, inp, gpu_results(w, desc, params))
+
+
 def test_paper_operating_point_g8(cuda_ok):
     """w = 16 with G = 8 (Qwen3-32B-like head ratio), tcgen05 path."""
     cfg = scaled(CONFIGS["paper_op"], L=1, h_kv=2, h_q=16, seq_lens=[2304, 2049], wave=0, free_slack=3)
