@@ -34,6 +34,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <type_traits>
 
 #include <cuda_bf16.h>
@@ -123,6 +124,7 @@ struct CoopArgs {
   float* part;     // [units][cmax][G*w] partial log2-sum-exp of each chunk (log2 domain, scaled logits)
   int* cnt;        // [units][2] chunks of the unit published, per CTA rank (column half)
   int* rs;         // [units + 2] first work index of each round; rs[nr] = units; rs[units + 1] = nr
+  int ktma;        // K tiles by TMA (b a power of two in 16..256), else the cp.async gather
   int lh_major;    // work order: 0 unit order (request-major); 1 (layer, head)-major, requests inner (shared
                    // prefix calls: the same (l, h) of many requests run at once, so their common prefix tiles
                    // are read from DRAM about once and from L2 by the others -- the prefix dedup)
@@ -290,7 +292,8 @@ __global__ void __launch_bounds__(1024) k_coop_plan(Call c, CoopArgs a) {
 
 // ------------------------------------------------------------------ the kernel
 template <int G, int W, int D>
-__global__ void __launch_bounds__(kCThreads, 1) k_score_coop(Call c, CoopArgs a, const __grid_constant__ CUtensorMap tmap_q) {
+__global__ void __launch_bounds__(kCThreads, 1) k_score_coop(Call c, CoopArgs a, const __grid_constant__ CUtensorMap tmap_q,
+                                                             const __grid_constant__ CUtensorMap tmap_k) {
   using K = CfgC<G, W, D>;
   if (*c.status != ZPC_OK) return;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -322,7 +325,8 @@ __global__ void __launch_bounds__(kCThreads, 1) k_score_coop(Call c, CoopArgs a,
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < K::ST; ++s) {
-      mbar_init(full0 + 8 * s, kCLoadWarps * 32 + (rank == 0 ? 1 : 0));   // + rank 1's relay
+      // the gather threads' cp.async arrivals, or (a.ktma) the feeder's one expect_tx arrival; + rank 1's relay
+      mbar_init(full0 + 8 * s, (a.ktma ? 1 : kCLoadWarps * 32) + (rank == 0 ? 1 : 0));
       mbar_init(empty0 + 8 * s, 1);
     }
     for (int i = 0; i < 4; ++i) { mbar_init(accf0 + 8 * i, 1); mbar_init(acce0 + 8 * i, i < 2 ? kCP1Warps : 2 * kCP2Warps); }
@@ -475,7 +479,7 @@ __global__ void __launch_bounds__(kCThreads, 1) k_score_coop(Call c, CoopArgs a,
         }
         __syncwarp();
       }
-    } else if (warp >= 4 && warp < 4 + kCLoadWarps) {
+    } else if (warp >= 4 && warp < 4 + kCLoadWarps && !a.ktma) {
       // ================= K gather of this CTA's 128 tokens of the step's pair-tile (16-B cp.async, SW128)
       constexpr int CPR = D / 8;
       constexpr int RPP = kCLoadWarps * 32 / CPR;
@@ -552,6 +556,7 @@ __global__ void __launch_bounds__(kCThreads, 1) k_score_coop(Call c, CoopArgs a,
     } else if (warp == 3) {
       // ================= feeder: walks the merged schedule (the only role that does), kIdAhead steps ahead:
       // step descriptor + chunk table entry + the tile's block ids; then the stage release
+      const uint64_t kpol = policy_evict_last();   // K tiles are re-read by pass 2
       Sched ls;
       ls.rho = 0; ls.nr = nr; ls.nch = ls.j1 = ls.k1 = ls.j2 = ls.k2 = ls.step = 0; ls.last = 1; ls.exhausted = false;
       const uint32_t ids_base = smem_u32(ids);
@@ -639,6 +644,40 @@ __global__ void __launch_bounds__(kCThreads, 1) k_score_coop(Call c, CoopArgs a,
           __syncwarp();
         }
         asm volatile("cp.async.wait_group %0;" ::"n"(kIdAhead) : "memory");
+        if (a.ktma) {
+          // K by TMA (b a power of two in 16..256): one box of R = min(b, 128) consecutive slots x 64 elements
+          // of head h per block the CTA's 128 tokens touch, per slab, straight into the SW128 K-major stage
+          __syncwarp();
+          const uint32_t dsc = desc[g % kDescRing];
+          if (lane == 0) {
+            const int st = g % K::ST;
+            if (dsc == kDescEnd) {
+              mbar_arrive(full0 + 8 * st);          // lets the MMA / relay see the end
+            } else {
+              const int k = (dsc >> 3) & 0xFFF, j = (int)(dsc >> 15);
+              const volatile int* ce = ctab + kCtabInts * (j & 7);
+              const int T = ce[0], l = ce[2], h = ce[3], tb = ce[4];
+              const int t0 = (tb + k) * 2 * kTile + rank * kTile;
+              const int R = min(c.b, kTile);
+              const int nbox = t0 < T ? (min(t0 + kTile, T) - 1) / R - t0 / R + 1 : 0;
+              mbar_expect_tx(full0 + 8 * st, (uint32_t)(nbox * K::SLABS * R * 128));
+              const uint32_t sid = ids_base + (uint32_t)(g % kIdSlots) * kMaxIds * 4;
+              const uint32_t dst0 = smem_u32(Ks + st * K::STAGE_BYTES);
+              for (int x = 0; x < nbox; ++x) {
+                const int tt = t0 + x * R;          // first token of box x
+                const int blk = lds_s32(sid + 4u * (uint32_t)(tt / c.b - t0 / c.b));
+                ZPC_CHECK(blk >= 0 && blk < c.N_total);
+                const int row = (l * c.N_total + blk) * c.b + tt % c.b;
+                for (int sl = 0; sl < K::SLABS; ++sl)
+                  tma_load_3d(dst0 + sl * K::SLAB_K + (uint32_t)(x * R * 128), &tmap_k, sl * 64, h, row,
+                              full0 + 8 * st, kpol);
+              }
+            }
+          }
+          __syncwarp();
+          if (dsc == kDescEnd) break;
+          continue;
+        }
         named_bar(4, kCLoadWarps * 32 + 32);
         if (desc[g % kDescRing] == kDescEnd) break;
       }
@@ -908,6 +947,23 @@ cudaError_t launch_coop_t(const Call& c, cudaStream_t s) {
           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
+  // K as [rows = L*N_total*b][h_kv][d]; one box = min(b, 128) consecutive slots x 64 elements of one head
+  CUtensorMap tk;
+  memset(&tk, 0, sizeof(tk));
+  int ktma = 0;
+#ifndef ZPC_COOP_TMA
+#define ZPC_COOP_TMA 1
+#endif
+  // only for blocks of >= 128 slots: with b = 16 a tile is 16 boxes of 16 rows per CTA and the TMA path measured
+  // 15.0 ms on the qwen7b batch against 8.2-8.5 for the cp.async gather (tuning build, one B200)
+  if (ZPC_COOP_TMA && c.b >= 128 && c.b <= 256 && (c.b & (c.b - 1)) == 0) {
+    const cuuint64_t kdim[3] = {(cuuint64_t)c.d, (cuuint64_t)c.h_kv, (cuuint64_t)c.L * c.N_total * c.b};
+    const cuuint64_t kstr[2] = {(cuuint64_t)c.d * 2, (cuuint64_t)c.h_kv * c.d * 2};
+    const cuuint32_t kbox[3] = {64, 1, (cuuint32_t)std::min(c.b, kTile)};
+    ktma = enc(&tk, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, c.k_cache, kdim, kstr, kbox, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+           CUDA_SUCCESS;
+  }
   auto kern = k_score_coop<G, W, D>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K::SMEM);
   if (e != cudaSuccess) return e;
@@ -958,6 +1014,10 @@ cudaError_t launch_coop_t(const Call& c, cudaStream_t s) {
   // Kept as a tuning switch; the dedup that pays needs the prefix tiles multiplied once against all the
   // sharing requests' queries.
   ca.lh_major = 0;
+  ca.ktma = ktma;
+#ifdef ZPC_TUNING
+  if (const char* e = getenv("ZPC_COOP_KTMA")) ca.ktma = std::min(ktma, atoi(e));
+#endif
 #ifdef ZPC_TUNING
   if (const char* e = getenv("ZPC_COOP_LHMAJOR")) ca.lh_major = atoi(e);
 #endif
@@ -969,7 +1029,7 @@ cudaError_t launch_coop_t(const Call& c, cudaStream_t s) {
   k_coop_plan<<<1, 1024, 0, s>>>(c, ca);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   cfg.gridDim = dim3((unsigned)(2 * npairs));
-  return cudaLaunchKernelEx(&cfg, kern, c, ca, tq);
+  return cudaLaunchKernelEx(&cfg, kern, c, ca, tq, tk);
 }
 
 template <int D>
