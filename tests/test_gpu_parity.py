@@ -235,6 +235,19 @@ def test_many_units_per_cluster(cuda_ok, monkeypatch, variant, shape):
     _run(cfg, seed=11 + G)
 
 
+# k_score_coop with K tiles by TMA (blocks of >= 128 slots): b = 128 and 256, ragged lengths
+@pytest.mark.parametrize("b,n_max", [(128, 5), (256, 3)])
+def test_coop_tma_blocks(cuda_ok, b, n_max):
+    cfg = scaled(CONFIGS["qwen7b"], L=2, h_kv=2, h_q=14, b=b, n_max=n_max, seq_lens=[1100, 700, 1500], budget=(32, 256),
+                 wave=0, free_slack=4)
+    w = from_host(make_host_workload(cfg, 60 + b))
+    desc, params = desc_params(w)
+    assert zipc.zpc_score_path(desc, params) == zipc.ZPC_PATH_COOP
+    inp = snapshot_inputs(w)
+    desc, params = run_gpu(w)
+    full_check(w, inp, gpu_results(w, desc, params))
+
+
 # MHA (G = 1) and the GQA ratios without a config (G = 2, 3, 6) on the tensor-core path (k_score_tc), at
 # d = 128 and d = 64; the library reports which scoring kernel family a call takes (zpc_score_path)
 @pytest.mark.parametrize("d", [128, 64])
