@@ -210,31 +210,35 @@ def max_over_ranks(value, dist=None, device=None):
 
 
 # ---------------------------------------------------------------- measured DRAM traffic
-TRAFFIC_FILE = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r02_traffic.json")
+PROFILES = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles")
+# committed `ncu --set full` captures of the bench's exact launches (scripts/ncu_capture.sh)
+TRAFFIC_FILES = {("qwen7b", False): "r02_traffic.json", ("qwen7b", True): "r02_traffic_lse.json",
+                 ("paper_op", False): "r02_traffic_paper_op.json"}
 
 
 def measured_traffic(cfg, per_gpu, lse_input=False):
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu --set full capture
-    of this exact workload (profiles/r02_traffic.json: the full qwen7b batch, 64 requests;
-    profiles/r01_traffic_lse.json: the same with --lse-input), else {}."""
-    path = TRAFFIC_FILE.replace("r02_traffic.json", "r01_traffic_lse.json") if lse_input else TRAFFIC_FILE
-    if cfg.name != "qwen7b" or per_gpu != 64 or not os.path.exists(path):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the score, compaction and redundancy kernels
+    from the committed capture of this exact workload (the config's default wave), else {}."""
+    f = TRAFFIC_FILES.get((cfg.name, bool(lse_input)))
+    if f is None or per_gpu != (cfg.wave or cfg.R):
         return {}
     try:
-        kern = json.load(open(path))["kernels"]
+        kern = json.load(open(os.path.join(PROFILES, f)))["kernels"]
     except (OSError, ValueError, KeyError):
         return {}
     out = {}
     for name, rec in kern.items():
         tot = rec["dram_bytes_read"] + rec["dram_bytes_write"]
-        if any(f"{k}<{cfg.h_q // cfg.h_kv}, {cfg.w}, {cfg.d}" in name for k in ("k_score_tc", "k_score_ovl", "k_score_coop")):
+        if "k_score" in name and f"<{cfg.h_q // cfg.h_kv}, {cfg.w}, {cfg.d}" in name:
             out["score"] = tot
         elif "k_compact" in name:
             out["compact"] = tot
+        elif "k_red_" in name:
+            out["redundancy"] = tot
     return out
 
 
-def redundancy_roofline(cfg, seq_lens, world, red_ms, peaks):
+def redundancy_roofline(cfg, seq_lens, world, red_ms, peaks, traffic=None):
     """NEXT-1 stage: reads K once (T*d*e per unit) and writes r (4T per unit): HBM-bound."""
     e = 2 if cfg.dtype == "bf16" else 4
     T = np.asarray(seq_lens, np.int64)
@@ -250,7 +254,7 @@ def redundancy_roofline(cfg, seq_lens, world, red_ms, peaks):
     flops = int(2 * cfg.b * cfg.d * (-(-T // cfg.b) * cfg.b).sum() * cfg.L * cfg.h_kv)
     return {"kernel": kern, "bound": "hbm",
             "achieved": ach, "peak": peaks["hbm"], "unit": "GB/s", "frac": ach / peaks["hbm"] if ach else None,
-            "algorithmic_bytes_per_launch": byts, "ms": red_ms,
+            "algorithmic_bytes_per_launch": byts, "ms": red_ms, "traffic": traffic,
             "gram_tflops": flops / (red_ms / 1e3) / 1e12 if red_ms else None}
 
 
@@ -367,7 +371,8 @@ def main():
     dev = torch.device("cuda", torch.cuda.current_device())
 
     from paper_2603_08743_b200 import zipc
-    from paper_2603_08743_b200.batch import batch_of, desc_params, window_lse_from_two_pass
+    from paper_2603_08743_b200.batch import batch_of, desc_params
+    from zpc_harness import window_lse_from_two_pass
     from zpc_inputs.device import generate
 
     rids = shard_rids(rank, world, per_gpu, cfg.R, args.scaling)
@@ -509,7 +514,7 @@ def main():
         "step_hbm_frac": step_bytes / (ms_per_step / 1e3) / 1e9 / peaks["hbm"],
         **({"redundancy_roofline": redundancy_roofline(cfg, lay.seq_lens, world,
                                                         stage_ms[stage_names.index("redundancy")] / args.steps,
-                                                        peaks)} if args.redundancy else {}),
+                                                        peaks, traffic.get("redundancy"))} if args.redundancy else {}),
         "kv_tokens_per_s": T_all / (ms_per_step / 1e3),
         "ranks": ranks, "output_checksum": job_checksum,
         **({"cuda_graph": graph_info} if graph_info else {}),

@@ -1,8 +1,15 @@
-# One ncu --set full capture of the bench's exact launch (the full qwen7b batch) for the roofline traffic,
-# plus the launch list of the bench command. Run on the GPU box: gpurun -- bash scripts/ncu_capture.sh
+# ncu --set full captures of the dominant kernels at the bench's exact launches (qwen7b: k_score_coop, k_select_reg,
+# k_compact; paper_op: k_score_res, k_red_umma) -> traffic records for bench.py. Run on the GPU box:
+#   gpurun -- bash scripts/ncu_capture.sh
 O=gpurun_out
+mkdir -p $O
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_score|k_compact|k_select" -c 3 \
   -o $O/prof_full -f python scripts/profile_step.py --requests 64 > $O/prof_full.log 2>&1
-ncu -i $O/prof_full.ncu-rep --page raw --csv --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed,lts__t_sector_hit_rate.pct,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active,sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active,smsp__issue_active.avg.pct_of_peak_sustained_active,sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active > $O/prof_full_raw.csv 2>&1
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches.csv \
-  python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > $O/launches_bench.log 2>&1
+python scripts/ncu_to_traffic.py $O/prof_full.ncu-rep "ncu --set full --import-source on --clock-control none -k regex:'k_score|k_compact|k_select' -c 3 python scripts/profile_step.py --requests 64 (the bench's qwen7b batch)" $O/traffic.json > /dev/null
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_score_res|k_red_umma|k_compact" -c 3 \
+  -o $O/prof_po -f python scripts/profile_step.py --config paper_op --requests 4 --redundancy > $O/prof_po.log 2>&1
+python scripts/ncu_to_traffic.py $O/prof_po.ncu-rep "ncu --set full --import-source on --clock-control none -k regex:'k_score_res|k_red_umma|k_compact' -c 3 python scripts/profile_step.py --config paper_op --requests 4 --redundancy" $O/traffic_paper_op.json > /dev/null
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_score" -c 1 \
+  -o $O/prof_lse -f python scripts/profile_step.py --requests 64 --lse-input > $O/prof_lse.log 2>&1
+python scripts/ncu_to_traffic.py $O/prof_lse.ncu-rep "ncu --set full -k regex:k_score -c 1 python scripts/profile_step.py --requests 64 --lse-input" $O/traffic_lse.json > /dev/null
+ls -la $O/*.json

@@ -29,7 +29,7 @@ cfg = CONFIGS[a.config]
 w = generate(cfg, 2603, np.arange(a.requests))
 flags = zipc.ZPC_F_SCORE_CUDACORE if a.cudacore else 0
 if a.lse_input:
-    from paper_2603_08743_b200.batch import window_lse_from_two_pass
+    from zpc_harness import window_lse_from_two_pass
     w.window_lse = window_lse_from_two_pass(w, flags)
 desc, params = desc_params(w, flags=flags, redundancy=(0.2, 0.4, 0.8) if a.redundancy else None,
                            lse_input=a.lse_input)

@@ -50,7 +50,7 @@ def run(name):
         hw.f_cache, hw.is_compressed = global_history(cfg, 7, hw.layout.N_total, hw.layout.rids)
     w = from_host(hw)
     if o.get("lse"):
-        from paper_2603_08743_b200.batch import window_lse_from_two_pass
+        from zpc_harness import window_lse_from_two_pass
         w.window_lse = window_lse_from_two_pass(w, 0)
     desc, params = desc_params(w, flags=o.get("flags", 0), redundancy=o.get("redundancy"),
                                global_alpha=o.get("global_alpha"), lse_input=bool(o.get("lse")))

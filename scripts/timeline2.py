@@ -9,7 +9,7 @@ from zpc_inputs.device import generate
 w = generate(CONFIGS["qwen7b"], 2603, np.arange(int(sys.argv[1]) if len(sys.argv) > 1 else 16))
 LSE = os.environ.get("TL_LSE") == "1"    # NEXT-4 single-pass mode: every step is a pass-2 step
 if LSE:
-    from paper_2603_08743_b200.batch import window_lse_from_two_pass
+    from zpc_harness import window_lse_from_two_pass
     w.window_lse = window_lse_from_two_pass(w)
 desc, params = desc_params(w, lse_input=LSE)
 b = batch_of(w, desc, params)

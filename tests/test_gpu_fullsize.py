@@ -205,7 +205,7 @@ def test_redundancy_sampled_units_vs_oracle(run7b_red, r, l, h):
 def run7b_lse():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
-    from paper_2603_08743_b200.batch import window_lse_from_two_pass
+    from zpc_harness import window_lse_from_two_pass
     cfg = CONFIGS["qwen7b"]
     w = generate(cfg, 2603, np.arange(cfg.R))
     tables0 = w.layout.tables.copy()
