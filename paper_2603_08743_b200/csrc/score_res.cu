@@ -391,6 +391,7 @@ __global__ void __launch_bounds__(kRThreads, 1) k_score_res(Call c, const __grid
     // while the current one is processed. wait_full: wait for each tile's MMA (first sweep); release: the
     // group's last read of each slot (last sweep).
     auto sweep = [&](const UnitInfo& u, int kt0, bool wait_full, bool release, auto&& on_chunk) {
+      if (u.nt == 0) return;                 // a short unit can leave a rank without tiles (R34)
       float va[32], vb[32];
       if (wait_full) { mbar_wait(sfull0 + 8 * (kt0 % K::NS), (kt0 / K::NS) & 1); tc_fence_after(); }
       ld32(kt0, 0, va);

@@ -82,6 +82,19 @@ def test_paper_operating_point_shape(cuda_ok, flags):
     _run(cfg, seed=8, flags=flags)
 
 
+def test_paper_op_short_units_empty_ranks(cuda_ok):
+    """k_score_res sizes its cluster by the longest unit (T = 2500 -> 6 ranks); a short unit in the same call
+    (T = 300: 3 tiles) leaves ranks without tiles, which must publish an empty (max, sum) and score nothing."""
+    cfg = scaled(CONFIGS["paper_op"], L=2, h_kv=2, h_q=8, b=128, n_max=3, seq_lens=[300, 2500, 1000], budget=(16, 256),
+                 wave=0, free_slack=4)
+    w = from_host(make_host_workload(cfg, 9))
+    desc, params = desc_params(w)
+    assert zipc.zpc_score_path(desc, params) == zipc.ZPC_PATH_RESIDENT
+    inp = snapshot_inputs(w)
+    desc, params = run_gpu(w)
+    full_check(w, inp, gpu_results(w, desc, params))
+
+
 def test_paper_op_normaliser_overflow_path(cuda_ok):
     """k_score_res's one-sweep normaliser uses the logit of each warp's first token as the exp2 reference; a
     logit ~100 log2 units above it must send the unit to the exact max-then-sum path. Key rows scaled by 2^6
