@@ -320,6 +320,8 @@ def main():
     ap.add_argument("--wave", type=int, default=0, help="requests per call per GPU (default: the config's)")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="weak: per_gpu requests on every rank; strong: the one-GPU batch split over the ranks")
+    ap.add_argument("--select-kernel", default="auto", choices=["auto", "smem", "reg"],
+                    help="A/B: params.variant select override (k_select / k_select_reg)")
     ap.add_argument("--graph", action="store_true",
                     help="NEXT-3: replay the whole step as one captured CUDA graph (launch-bound small batches); "
                          "value/ms_per_step then come from the graph replays, stage_ms from the eager steps")
@@ -373,6 +375,8 @@ def main():
     from paper_2603_08743_b200 import zipc
     from paper_2603_08743_b200.batch import batch_of, desc_params
     from zpc_harness import window_lse_from_two_pass
+    if args.select_kernel != "auto":
+        zipc.DEFAULT_VARIANT = zipc.variant(select={"smem": 1, "reg": 2}[args.select_kernel])
     from zpc_inputs.device import generate
 
     rids = shard_rids(rank, world, per_gpu, cfg.R, args.scaling)

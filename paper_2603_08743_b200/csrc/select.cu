@@ -468,7 +468,8 @@ cudaError_t launch_select(const Call& c, cudaStream_t s) {
       kern<<<units, nt, smem, s>>>(c);
       return cudaGetLastError();
     };
-    // 32 keys per thread and a CTA that shrinks with T, so 8K units run 3 CTAs per SM
+    // 32 keys per thread and a CTA that shrinks with T, so 8K units run 3 CTAs per SM; 16 keys for T <= 4K
+    if (T <= 16 * 256) return launch(k_select_reg<256, 16>, 256);
     if (T <= 32 * 256) return launch(k_select_reg<256, 32>, 256);
     if (T <= 32 * 512) return launch(k_select_reg<512, 32>, 512);
     return launch(k_select_reg<1024, 32>, 1024);
