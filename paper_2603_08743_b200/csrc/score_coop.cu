@@ -260,10 +260,16 @@ __device__ __forceinline__ int ld_acquire_s32(const int* p) {
 // ------------------------------------------------------------------ plan kernel
 // Rounds of whole units, packed greedily in unit order onto `npairs` slots; each unit of request r has
 // c_r = ceil(ceil(T_r/256) / kt) chunks. Also zeroes the arrival counters.
+constexpr int kPlanStageR = 8192;   // requests whose chunk counts are staged in shared memory first
 __global__ void __launch_bounds__(1024) k_coop_plan(Call c, CoopArgs a) {
   if (*c.status != ZPC_OK) return;
+  __shared__ int crs[kPlanStageR];    // chunk count per request (the serial packing loop reads no global memory)
   const int HU = c.L * c.h_kv, units = c.R * HU;
   for (int i = threadIdx.x; i < 2 * units; i += blockDim.x) a.cnt[i] = 0;
+  const bool staged = c.R <= kPlanStageR;
+  if (staged)
+    for (int r = threadIdx.x; r < c.R; r += blockDim.x) crs[r] = max(((c.seq_lens[r] + 255) / 256 + a.kt - 1) / a.kt, 1);
+  __syncthreads();
   if (threadIdx.x == 0) {
     int rho = 0, used = 0;
     a.rs[0] = 0;
@@ -271,9 +277,7 @@ __global__ void __launch_bounds__(1024) k_coop_plan(Call c, CoopArgs a) {
     const int nruns = a.lh_major ? units : c.R;
     for (int run = 0; run < nruns; ++run) {
       const int r = a.lh_major ? run % c.R : run;
-      const int T = c.seq_lens[r];
-      const int npt = (T + 255) >> 8;
-      const int cr = max((npt + a.kt - 1) / a.kt, 1);
+      const int cr = staged ? crs[r] : max(((c.seq_lens[r] + 255) / 256 + a.kt - 1) / a.kt, 1);
       if (cr > a.npairs) { *c.status = ZPC_ERR_SEQ_TOO_LONG; return; }   // host sized kt from max_seq_len
       int u = a.lh_major ? run : r * HU, m = a.lh_major ? 1 : HU;
       while (m > 0) {
