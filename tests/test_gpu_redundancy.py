@@ -87,6 +87,9 @@ CASES = {
                             free_slack=5),
     "bf16_b256_tile": scaled(CONFIGS["paper_op"], L=2, h_kv=2, h_q=8, seq_lens=[2304, 2149], budget=2048, wave=0,
                              free_slack=4),
+    # more blocks than SMs: every SM runs several k_red_umma CTAs over the call
+    "bf16_b256_many": scaled(CONFIGS["paper_op"], L=4, h_kv=8, h_q=32, seq_lens=[2304, 2149, 2304, 2500], budget=2048,
+                             wave=0, free_slack=6),
     "bf16_b48_d64_tile": scaled(CONFIGS["qwen32b"], L=1, h_kv=2, h_q=10, d=64, b=48, n_max=6, seq_lens=[250, 290],
                                 budget=200, wave=0, free_slack=4),
 }
