@@ -61,7 +61,10 @@ static_assert(8 * kCProdRegs + kCP1Warps * kCP1Regs + kCP2Warps * kCP2Regs <= 20
 #define ZPC_COOP_DELTA 12 // merged steps between a chunk's last pass-1 step and its first pass-2 step
 #endif
 #ifndef ZPC_COOP_KT
-#define ZPC_COOP_KT 16    // pair-tiles per chunk (>= kCoopChunkTiles)
+// pair-tiles per chunk (>= kCoopChunkTiles). Measured (production builds, one B200, score ms for kt = 16 / 32 /
+// 64): qwen7b 7.69 / 7.48 / 7.47, qwen32b 34.2 / 33.3 / 32.5, prefix 23.3 / 22.4 / 22.0 (128 and 512 within noise
+// of 64): whole units per pair beat splitting a unit across pairs, so chunks only split units past 16K tokens.
+#define ZPC_COOP_KT 64
 #endif
 #ifndef ZPC_COOP_HINTS
 #define ZPC_COOP_HINTS 0  // CoopArgs::hints
