@@ -13,105 +13,17 @@
 // (launch_compact).
 #include <cstdlib>
 
+#include "compact_dev.h"
 #include "internal.h"
 
 namespace zpc {
 namespace {
 
 
-template <int VPR, int kVec>
-struct Chunk {
-  int4 k[kVec], v[kVec];
-  uint32_t dst[kVec];                // destination vector index within the layer-head plane, ~0u = none
-  float f[kVec];                     // NEXT-2: the row's global score (the row's first vector carries it)
-  uint32_t fdst[kVec];               // its destination row (blk*b + slot), ~0u = none
-};
-
-template <int VPR, int kVec, int kThreads>
-__device__ __forceinline__ void load_chunk(const Call& c, Chunk<VPR, kVec>& ch, int base, int ell, const int32_t* kept,
-                                           const int32_t* table, const int32_t* tg, const int4* K, const int4* V,
-                                           size_t plane, int bsh, const float* F, size_t fplane) {
-  constexpr int CH = kVec * kThreads / VPR;        // ranks per chunk
-  const int nvec = min(CH, ell - base) * VPR;
-  const uint32_t rowv = (uint32_t)c.h_kv * VPR;    // vectors between consecutive slots
-#pragma unroll
-  for (int k = 0; k < kVec; ++k) {
-    const int v = threadIdx.x + k * kThreads;
-    ch.dst[k] = ~0u;
-    if (v < nvec) {
-      const int i = base + v / VPR, e = v % VPR;
-      const int t = kept[i];
-      int sblk, sslot, dblk, dslot;
-      if (bsh >= 0) {
-        sblk = table[t >> bsh]; sslot = t & ((1 << bsh) - 1);
-        dblk = tg[i >> bsh];    dslot = i & ((1 << bsh) - 1);
-      } else {
-        sblk = table[t / c.b]; sslot = t % c.b;
-        dblk = tg[i / c.b];    dslot = i % c.b;
-      }
-      ZPC_CHECK(t >= i && sblk >= 0 && sblk < c.N_total && dblk >= 0 && dblk < c.N_total);
-      // vector index relative to the (layer, head) plane: (blk*b + slot)*h_kv*VPR + e
-      const uint32_t src = ((uint32_t)sblk * c.b + sslot) * rowv + e;
-      const uint32_t d = ((uint32_t)dblk * c.b + dslot) * rowv + e;
-      ch.fdst[k] = ~0u;
-      if (src != d) {
-        ch.k[k] = K[plane + src];
-        ch.v[k] = V[plane + src];
-        ch.dst[k] = d;
-        if (F && e == 0) {            // F moves with its K/V row
-          ch.f[k] = F[fplane + ((size_t)sblk * c.b + sslot) * c.h_kv];
-          ch.fdst[k] = (uint32_t)dblk * c.b + dslot;
-        }
-      }
-    }
-  }
-}
-
 template <int VPR, int kVec, int kThreads, int kMinCtas>
 __global__ void __launch_bounds__(kThreads, kMinCtas) k_compact(Call c) {
   if (*c.status != ZPC_OK) return;
-  constexpr int CH = kVec * kThreads / VPR;
-  const int unit = blockIdx.x;
-  const int h = unit % c.h_kv;
-  const int l = (unit / c.h_kv) % c.L;
-  const int r = unit / (c.h_kv * c.L);
-  const int ell = c.new_lens[unit];
-  const int nm1 = c.n_max - 1;
-  const int32_t* kept = c.ws.kept + (size_t)unit * c.ws.kept_stride;
-  const int32_t* tg = c.ws.targets + (size_t)r * nm1;
-  const int32_t* table = c.tables + (size_t)r * c.table_stride;
-  const int bsh = (c.b & (c.b - 1)) == 0 ? __ffs(c.b) - 1 : -1;
-  const int4* K = reinterpret_cast<const int4*>(c.k_cache);
-  const int4* V = reinterpret_cast<const int4*>(c.v_cache);
-  int4* Kw = reinterpret_cast<int4*>(c.k_cache);
-  int4* Vw = reinterpret_cast<int4*>(c.v_cache);
-  // start of the (layer l, head h) plane in vectors; per-row offsets are 32-bit within a layer
-  const size_t plane = (size_t)l * c.N_total * c.b * c.h_kv * VPR + (size_t)h * VPR;
-  float* Fw = (c.flags & ZPC_F_GLOBAL_SCORE) ? c.f_cache : nullptr;   // NEXT-2 relocation
-  const size_t fplane = (size_t)l * c.N_total * c.b * c.h_kv + h;
-  unsigned moved = 0;
-
-  Chunk<VPR, kVec> cur, nxt;
-  if (ell > 0) load_chunk<VPR, kVec, kThreads>(c, cur, 0, ell, kept, table, tg, K, V, plane, bsh, Fw, fplane);
-  for (int base = 0; base < ell; base += CH) {
-    __syncthreads();   // every read of chunk `base` has returned before any write of it
-    const bool more = base + CH < ell;
-    if (more) load_chunk<VPR, kVec, kThreads>(c, nxt, base + CH, ell, kept, table, tg, K, V, plane, bsh, Fw, fplane);
-#pragma unroll
-    for (int k = 0; k < kVec; ++k) {
-      if (cur.dst[k] != ~0u) {
-        Kw[plane + cur.dst[k]] = cur.k[k];
-        Vw[plane + cur.dst[k]] = cur.v[k];
-        if (cur.fdst[k] != ~0u) Fw[fplane + (size_t)cur.fdst[k] * c.h_kv] = cur.f[k];
-        moved += ((threadIdx.x + k * kThreads) % VPR) == 0;
-      }
-    }
-    if (more) cur = nxt;
-  }
-  if (c.flags & ZPC_F_COUNT_MOVES) {
-    for (int o = 16; o; o >>= 1) moved += __shfl_xor_sync(0xffffffffu, moved, o);
-    if ((threadIdx.x & 31) == 0 && moved) atomicAdd(c.ws.moves, (unsigned long long)moved);
-  }
+  compact_unit<VPR, kVec, kThreads>(c, blockIdx.x);
 }
 
 }  // namespace

@@ -276,8 +276,7 @@ __device__ float block_sum_t(float v, float* sm) {
 __device__ __forceinline__ int pidx(int t) { return t + (t >> 5); }
 
 template <int NT, int CH>
-__global__ void __launch_bounds__(NT) k_select_reg(Call c) {
-  if (*c.status != ZPC_OK) return;
+__device__ __forceinline__ void select_reg_unit(const Call& c, const int unit) {
   extern __shared__ float sS[];                 // [pidx(T)] staged S (padded)
   __shared__ int hist[256];
   __shared__ int sm[NT / 32];
@@ -285,7 +284,6 @@ __global__ void __launch_bounds__(NT) k_select_reg(Call c) {
   __shared__ uint32_t s_prefix;
   __shared__ int s_need;
 
-  const int unit = blockIdx.x;
   const int h = unit % c.h_kv;
   const int l = (unit / c.h_kv) % c.L;
   const int r = unit / (c.h_kv * c.L);
@@ -446,6 +444,12 @@ __global__ void __launch_bounds__(NT) k_select_reg(Call c) {
 #pragma unroll
   for (int i = 0; i < CH; ++i)
     if (keepm >> i & 1u) { ZPC_CHECK(o < ell && t0 + i < T); out[o++] = t0 + i; }
+}
+
+template <int NT, int CH>
+__global__ void __launch_bounds__(NT) k_select_reg(Call c) {
+  if (*c.status != ZPC_OK) return;
+  select_reg_unit<NT, CH>(c, blockIdx.x);
 }
 
 }  // namespace
