@@ -30,6 +30,7 @@ sys.path.insert(0, ROOT)
 
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_HBM_GBS = 6650.0
+NOMINAL_HBM_GBS = 8000.0   # B200 data-sheet HBM3e bandwidth (report the measured and the nominal peak)
 FALLBACK_BF16_TFLOPS = 1590.0
 
 
@@ -274,7 +275,7 @@ def score_roofline(ab, passes, score_ms, peaks, traffic):
     flops = ab["flops_score"] * passes
     hbm_gbs = ab["score"] / secs / 1e9
     hbm = {"achieved": hbm_gbs, "peak": peaks["hbm"], "unit": "GB/s", "frac": hbm_gbs / peaks["hbm"],
-           "algorithmic_bytes_per_launch": ab["score"]}
+           "frac_of_nominal_8TBs": hbm_gbs / NOMINAL_HBM_GBS, "algorithmic_bytes_per_launch": ab["score"]}
     ridge = peaks["bf16"] * 1e12 / (peaks["hbm"] * 1e9)
     intensity = flops / ab["score"]
     base = {"kernel": "score (a1+a2)", "passes": passes, "intensity_flop_per_byte": intensity,
@@ -540,6 +541,7 @@ def main():
                              "frac": (ab["compact"] / (compact_ms / 1e3) / 1e9) / peaks["hbm"] if compact_ms else None,
                              "traffic": traffic.get("compact"), "algorithmic_bytes_per_launch": ab["compact"]},
         "step_hbm_frac": step_bytes / (ms_per_step / 1e3) / 1e9 / peaks["hbm"],
+        "step_hbm_frac_of_nominal_8TBs": step_bytes / (ms_per_step / 1e3) / 1e9 / NOMINAL_HBM_GBS,
         **({"redundancy_roofline": redundancy_roofline(cfg, lay.seq_lens, world,
                                                         stage_ms[stage_names.index("redundancy")] / args.steps,
                                                         peaks, traffic.get("redundancy"))} if args.redundancy else {}),
