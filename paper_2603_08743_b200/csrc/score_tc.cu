@@ -220,9 +220,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
   // per-unit geometry, identical in every role
   // NEXT-4 (ZPC_F_LSE_INPUT): the normalisers are an input, so a unit runs only pass 2 (p1 = 0)
   const bool one_pass = c.lse_in != nullptr;
-  struct UnitInfo { int r, l, h, T, slot, tb, nt, p1; };
-  auto unit_info = [&](int unit) {
+  struct UnitInfo { int r, l, h, T, slot, tb, nt, p1, id; };
+  // work index -> unit: (layer, head)-major with the requests inner for single-pass shared-prefix calls, so the
+  // clusters working at the same time read the same prefix tiles (one DRAM read, the rest from L2: the prefix
+  // dedup of PAPER.md:131); unit order otherwise
+  const bool lh_major = one_pass && (c.flags & ZPC_F_PREFIX) && !(c.debug & 8192u);
+  auto unit_info = [&](int v) {
     UnitInfo u;
+    const int unit = lh_major ? (v % c.R) * (c.L * c.h_kv) + v / c.R : v;
+    u.id = unit;
     u.h = unit % c.h_kv;
     u.l = (unit / c.h_kv) % c.L;
     u.r = unit / (c.h_kv * c.L);
@@ -522,16 +528,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
             // h*G + g at window row u; log2 domain like pass 1's
             // (the next unit's value is loaded here too, so its latency is off the next boundary)
             if (col_ok) {
-              const float L2 = (it == 0 ? lse_input(unit) : lse_next) * kLog2e;
-              if (unit + nclusters < units) lse_next = lse_input(unit + nclusters);
+              const float L2 = (it == 0 ? lse_input(u.id) : lse_next) * kLog2e;
+              if (unit + nclusters < units) lse_next = lse_input(unit_info(unit + nclusters).id);
               write_aug(col, L2);
-              if (rank == 0) c.ws.lse[(size_t)unit * K::GW + col] = L2;
+              if (rank == 0) c.ws.lse[(size_t)u.id * K::GW + col] = L2;
             }
           } else if (C == 1) {
             if (col_ok) {
               const float L2 = m + lg2f(ssum);
               write_aug(col, L2);
-              c.ws.lse[(size_t)unit * K::GW + col] = L2;
+              c.ws.lse[(size_t)u.id * K::GW + col] = L2;
             }
           } else {
             if (col_ok) { pmv[pb * 256 + col] = m; psv[pb * 256 + col] = ssum; }
@@ -556,7 +562,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
                 if (mr[rr] > -INFINITY) S += sr[rr] * ex2f(mr[rr] - M);
               const float L2 = M + lg2f(S);
               write_aug(col, L2);
-              if (rank == 0) c.ws.lse[(size_t)unit * K::GW + col] = L2;
+              if (rank == 0) c.ws.lse[(size_t)u.id * K::GW + col] = L2;
             }
           }
           named_bar(1, kEpiWarps * 32);
@@ -683,7 +689,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
           if (c.debug & 1u) { const uint32_t ts2 = (uint32_t)gtimer(); tacc[3] += ts1 - ts0; tacc[4] += ts2 - ts1; }
           named_bar(1, kEpiWarps * 32);
           if (half == 0 && t < u.T && !(c.debug & 16384u))
-            c.ws.scores[(size_t)unit * c.max_seq_len + t] = (accs + cb[q * 32 + lane]) * (1.0f / W);
+            c.ws.scores[(size_t)u.id * c.max_seq_len + t] = (accs + cb[q * 32 + lane]) * (1.0f / W);
         }
         if (rec) dbg[8192 + astep * 4 + 2] = gtimer();
         if (c.debug & 1u) {
