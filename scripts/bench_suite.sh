@@ -12,6 +12,7 @@ timeout 600 python bench.py --config paper_op --graph --steps 50 --wave 1 --no-c
 timeout 600 python bench.py --config llama8b --no-cpu-baseline > $O/bench_llama8b.json 2> $O/bench_llama8b.err
 timeout 600 python bench.py --config qwen32b --no-cpu-baseline > $O/bench_qwen32b.json 2> $O/bench_qwen32b.err
 timeout 600 python bench.py --config prefix --no-cpu-baseline > $O/bench_prefix.json 2> $O/bench_prefix.err
+timeout 600 python bench.py --config prefix --lse-input --no-cpu-baseline > $O/bench_prefix_lse.json 2> $O/bench_prefix_lse.err
 timeout 600 python bench.py --scaling strong --no-cpu-baseline > $O/bench_strong1.json 2> $O/bench_strong1.err
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_reference.json 2> $O/bench_reference.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > $O/launches_bench.log 2>&1
