@@ -69,6 +69,7 @@ __global__ void __launch_bounds__(kRThreads, 3) k_red_umma(Call c, const __grid_
   float* zv = sq;                                   //        and that entry's value (both after the epilogues)
   uint64_t* bar = reinterpret_cast<uint64_t*>(zvpart + 512);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 2);   // bar[0] MMA, bar[1] TMA load
+  int* zflag = reinterpret_cast<int*>(tmem_slot + 1);           // some entry of the block is above p
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t base = smem_u32(smem);
   const uint32_t ncols = red_tmem_cols(b);
@@ -113,12 +114,15 @@ __global__ void __launch_bounds__(kRThreads, 3) k_red_umma(Call c, const __grid_
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
+    *zflag = 0;
     mbar_init(smem_u32(bar), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (ktma) {
     __syncthreads();                                // lbar initialised before anyone waits on it
-    mbar_wait(lbar, 0);
+    // one warp polls the barrier; the others block in bar.sync (no issue slots spent spinning)
+    if (warp == 0) mbar_wait(lbar, 0);
+    __syncthreads();
     if (nvalid < b) {                               // slots >= T of a partial last block: zero rows (R20)
       for (int q = tid; q < (b - nvalid) * (D / 8); q += kRThreads) {
         const int row = nvalid + q / (D / 8), ch = q % (D / 8);
@@ -181,7 +185,8 @@ __global__ void __launch_bounds__(kRThreads, 3) k_red_umma(Call c, const __grid_
         }
         umma_commit_elect(smem_u32(bar));
       }
-      mbar_wait(smem_u32(bar), (uint32_t)(nmma & 1));
+      if (warp == 0) mbar_wait(smem_u32(bar), (uint32_t)(nmma & 1));   // one poller, as above
+      __syncthreads();
       tc_fence_after();
       if (rows_ok) {
         const int ncw = N / 2;                      // this warp's columns: a multiple of 8
@@ -241,6 +246,7 @@ __global__ void __launch_bounds__(kRThreads, 3) k_red_umma(Call c, const __grid_
               if (j != i && cs > p) { zj = j; zval = cs; }
             }
           }
+          if (lane == 0) *zflag = 1;
         }
       }
       tc_fence_before();
@@ -260,6 +266,11 @@ __global__ void __launch_bounds__(kRThreads, 3) k_red_umma(Call c, const __grid_
     }
   }
   __syncthreads();
+  float* out = c.ws.redund + (size_t)unit * c.max_seq_len;
+  const float inv_T = 1.0f / (float)T;
+  if (*zflag == 0) {                                // the common case: no cosine above p in the block
+    for (int i = tid; i < nvalid; i += kRThreads) out[j0 + i] = (rsum[i] + rsum[256 + i]) * inv_T;
+  } else {
   // per column i: row i's last column above p (the larger column index of the two column-split warps)
   for (int i = tid; i < b; i += kRThreads) {
     const bool up = zpart[256 + i] > zpart[i];
@@ -268,8 +279,6 @@ __global__ void __launch_bounds__(kRThreads, 3) k_red_umma(Call c, const __grid_
   }
   __syncthreads();
   // remove each column's zeroed entry from its row, in ascending column order; r[t] = sum / T
-  float* out = c.ws.redund + (size_t)unit * c.max_seq_len;
-  const float inv_T = 1.0f / (float)T;
   for (int i0 = warp * 32; i0 < b; i0 += kRThreads) {
     const int i = i0 + lane;
     float s = i < b ? rsum[i] + rsum[256 + i] : 0.f;
@@ -285,6 +294,7 @@ __global__ void __launch_bounds__(kRThreads, 3) k_red_umma(Call c, const __grid_
       }
     }
     if (i < nvalid) out[j0 + i] = s * inv_T;
+  }
   }
   tc_fence_before();
   __syncthreads();
