@@ -63,7 +63,9 @@ static_assert(8 * kCProdRegs + kCP1Warps * kCP1Regs + kCP2Warps * kCP2Regs <= 20
 #ifndef ZPC_COOP_KT
 // pair-tiles per chunk (>= kCoopChunkTiles). Measured (production builds, one B200, score ms for kt = 16 / 32 /
 // 64): qwen7b 7.69 / 7.48 / 7.47, qwen32b 34.2 / 33.3 / 32.5, prefix 23.3 / 22.4 / 22.0 (128 and 512 within noise
-// of 64): whole units per pair beat splitting a unit across pairs, so chunks only split units past 16K tokens.
+// of 64); qwen7b at kt = 4 / 8 / 16 / 64 on one box: 9.26 / 8.83 / 8.32 / 7.96 (delta 4 / 24 at kt = 8: 8.88 /
+// 8.62): whole units per pair beat splitting a unit across pairs (the shorter pass-1 -> pass-2 distance does not
+// buy L2 hits), so chunks only split units past 16K tokens.
 #define ZPC_COOP_KT 64
 #endif
 #ifndef ZPC_COOP_HINTS

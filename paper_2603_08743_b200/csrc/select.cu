@@ -461,9 +461,14 @@ cudaError_t launch_select(const Call& c, cudaStream_t s) {
   const int mode = vsel == 0 ? 1 : (vsel == 1 ? 0 : 2);
   const bool reg = mode != 0;
   const int T = c.max_seq_len;
-  // T <= 4K (the paper's operating point, T = 2304): k_select measured faster (0.066 ms per 4-request
-  // call vs 0.078 with 1024 x 4 register keys and 0.114 with 256 x 32)
-  if (reg && (T > 4 * kThreads || mode == 2) && T <= 32 * kThreads) {
+  // T <= 4K (the paper's operating point, T = 2304): k_select_reg<256, 16> when there are >= 4 units per SM
+  // (paper_op, 4 requests, 1152 units: 0.041 ms vs 0.045 for k_select), k_select below that (1 request, 288
+  // units: 0.017 vs 0.019 -- 1024-thread CTAs spread a small call over more of the SMs)
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+    return cudaErrorInvalidDevice;
+  const bool many = units >= 4 * sms;
+  if (reg && (T > 4 * kThreads || mode == 2 || many) && T <= 32 * kThreads) {
     const size_t smem = sizeof(float) * (size_t)(T + T / 32 + 1);
     auto launch = [&](auto kern, int nt) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
