@@ -792,7 +792,7 @@ __global__ void __launch_bounds__(kCThreads, 1) k_score_coop(Call c, CoopArgs a,
 #pragma unroll 1
       for (int k = 0; k < A.nt; ++k, ++n1) {
         if (warp == kCEpi0 && lane == 0 && n1 < 1024) CTRACE(45056 + 4 * n1, clk32());
-        mbar_wait(accf0 + 8 * hs, (uint32_t)(n1 & 1));
+        mbar_wait_lean(accf0 + 8 * hs, (uint32_t)(n1 & 1));
         if (warp == kCEpi0 && lane == 0 && n1 < 1024) CTRACE(45056 + 4 * n1 + 1, clk32());
         tc_fence_after();
         // first token of this warp's 64: rank (tq & 1)'s K rows hs*64 .. of the pair-tile
@@ -887,7 +887,7 @@ __global__ void __launch_bounds__(kCThreads, 1) k_score_coop(Call c, CoopArgs a,
         float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll 1
         for (int h = 0; h < 2; ++h) {
-          mbar_wait(accf0 + 8 * (2 + h), (uint32_t)(n2 & 1));
+          mbar_wait_lean(accf0 + 8 * (2 + h), (uint32_t)(n2 & 1));
           tc_fence_after();
           if (CDEBUG(2)) {   // bisection: no pass-2 math
             tc_fence_before();

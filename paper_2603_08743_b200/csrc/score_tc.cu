@@ -577,7 +577,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_tc(Call c, const __grid_c
         // MMA(astep) complete: each warp waits the commit mbarrier itself (try_wait parks the warp;
         // no cross-warp barrier, so warps are not held to the slowest one every step). No phase
         // aliasing: MMA(astep + 2) needs every epilogue warp's acc_empty arrival for astep.
-        mbar_wait(accf0 + 8 * a, (astep >> 1) & 1);
+        mbar_wait_lean(accf0 + 8 * a, (astep >> 1) & 1);
         if (rec) dbg[8192 + astep * 4 + 1] = gtimer();
         const uint32_t ts0 = (c.debug & 1u) ? (uint32_t)gtimer() : 0u;   // per-warp register timing (mod 2^32)
         if (c.debug & 1u) { tacc[(i < u.p1 ? 0 : 3) + 2] += ts0 - tlast; }
@@ -1147,7 +1147,7 @@ __global__ void __launch_bounds__(kThreadsO, 1) k_score_ovl(Call c, const __grid
         auto pair = [&](int bp, auto mask_tag) {
           constexpr bool kMask = decltype(mask_tag)::value;
           const int a = n1 & 1;
-          mbar_wait(accf0 + 8 * a, (n1 >> 1) & 1);
+          mbar_wait_lean(accf0 + 8 * a, (n1 >> 1) & 1);
           tc_fence_after();
           ++n1;
 #pragma unroll
@@ -1166,7 +1166,7 @@ __global__ void __launch_bounds__(kThreadsO, 1) k_score_ovl(Call c, const __grid
         };
         if (!warp_cols) {
           for (int hs = 0; hs < kSub; ++hs, ++n1) {
-            mbar_wait(accf0 + 8 * (n1 & 1), (n1 >> 1) & 1);
+            mbar_wait_lean(accf0 + 8 * (n1 & 1), (n1 >> 1) & 1);
             tc_fence_after();
             tc_fence_before();
             __syncwarp();
@@ -1250,7 +1250,7 @@ __global__ void __launch_bounds__(kThreadsO, 1) k_score_ovl(Call c, const __grid
       const UnitInfo B = unit_info(j);
       const int unitB = cluster_id + j * nclusters;
       for (int k = 0; k < B.nt; ++k, ++n2) {
-        mbar_wait(accf0 + 16, n2 & 1);
+        mbar_wait_lean(accf0 + 16, n2 & 1);
         tc_fence_after();
         const int t0 = (B.tb + B.nt - 1 - k) * kTile;
         const int t = t0 + q * 32 + lane;
