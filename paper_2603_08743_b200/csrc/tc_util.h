@@ -77,7 +77,8 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 // instead of a 64-bit counter and a %globaltimer branch per poll. Measured (A/B on one B200): k_score_coop
 // qwen7b 7.53 -> 7.42 ms, k_score_tc --lse-input 3.60 -> 3.53, k_score_ovl llama8b 11.96 -> 11.92; k_score_res
 // paper_op 0.1758 -> 0.1765 (kept on mbar_wait); the same loop for every wait of every kernel 7.75 -> 9.07 ms
-// (producers without the hint spin).
+// (producers without the hint spin); the MMA issuers' and feeders' waits alone through lean loops: qwen7b
+// 7.57 -> 8.60, llama8b 12.1 -> 12.9 (their waits keep the hint).
 __device__ __forceinline__ void mbar_wait_lean(uint32_t bar, uint32_t parity) {
   for (uint32_t n = 0;; ++n) {
     uint32_t done;
