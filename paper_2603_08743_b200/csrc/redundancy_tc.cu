@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(kRThreads, 3) k_red_umma(Call c, const __grid_
   if (ktma) {
     __syncthreads();                                // lbar initialised before anyone waits on it
     // one warp polls the barrier; the others block in bar.sync (no issue slots spent spinning)
-    if (warp == 0) mbar_wait(lbar, 0);
+    if (warp == 0) mbar_wait_lean(lbar, 0);
     __syncthreads();
     if (nvalid < b) {                               // slots >= T of a partial last block: zero rows (R20)
       for (int q = tid; q < (b - nvalid) * (D / 8); q += kRThreads) {
@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(kRThreads, 3) k_red_umma(Call c, const __grid_
         }
         umma_commit_elect(smem_u32(bar));
       }
-      if (warp == 0) mbar_wait(smem_u32(bar), (uint32_t)(nmma & 1));   // one poller, as above
+      if (warp == 0) mbar_wait_lean(smem_u32(bar), (uint32_t)(nmma & 1));   // one poller, as above
       __syncthreads();
       tc_fence_after();
       if (rows_ok) {
