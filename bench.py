@@ -329,6 +329,8 @@ def main():
                     help="weak: per_gpu requests on every rank; strong: the one-GPU batch split over the ranks")
     ap.add_argument("--select-kernel", default="auto", choices=["auto", "smem", "reg"],
                     help="A/B: params.variant select override (k_select / k_select_reg)")
+    ap.add_argument("--compact-nt", type=int, default=0, choices=[0, 128, 256, 512, 1024],
+                    help="A/B: params.variant compaction CTA width override (0 = by unit count)")
     ap.add_argument("--graph", action="store_true",
                     help="NEXT-3: replay the whole step as one captured CUDA graph (launch-bound small batches); "
                          "value/ms_per_step then come from the graph replays, stage_ms from the eager steps")
@@ -385,8 +387,9 @@ def main():
     from paper_2603_08743_b200 import zipc
     from paper_2603_08743_b200.batch import batch_of, desc_params
     from zpc_harness import window_lse_from_two_pass
-    if args.select_kernel != "auto":
-        zipc.DEFAULT_VARIANT = zipc.variant(select={"smem": 1, "reg": 2}[args.select_kernel])
+    if args.select_kernel != "auto" or args.compact_nt:
+        zipc.DEFAULT_VARIANT = zipc.variant(select={"auto": 0, "smem": 1, "reg": 2}[args.select_kernel],
+                                            compact_nt=args.compact_nt)
     from zpc_inputs.device import generate
 
     rids = shard_rids(rank, world, per_gpu, cfg.R, args.scaling)

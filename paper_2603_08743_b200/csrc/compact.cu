@@ -20,10 +20,10 @@ namespace zpc {
 namespace {
 
 
-template <int VPR, int kVec, int kThreads, int kMinCtas>
+template <int VPR, int kVec, int kThreads, int kMinCtas, bool HasF, bool Ahead>
 __global__ void __launch_bounds__(kThreads, kMinCtas) k_compact(Call c) {
   if (*c.status != ZPC_OK) return;
-  compact_unit<VPR, kVec, kThreads>(c, blockIdx.x);
+  compact_unit<VPR, kVec, kThreads, HasF, Ahead>(c, blockIdx.x);
 }
 
 }  // namespace
@@ -46,12 +46,22 @@ cudaError_t launch_compact(const Call& c, cudaStream_t s) {
   int nt = units >= sms * 6 ? 256 : (units >= sms * 3 ? 512 : 1024);
   const uint32_t vnt = (c.variant >> ZPC_V_COMPACT_SHIFT) & 7u;   // params.variant override (tests, A/B)
   if (vnt != 0) nt = 64 << vnt;
-#define ZPC_COMPACT_CASE(VPR)                                                      \
-  case VPR:                                                                       \
-    if (nt == 128) k_compact<VPR, 1, 128, 16><<<units, 128, 0, s>>>(c);           \
-    else if (nt == 256) k_compact<VPR, 1, 256, 8><<<units, 256, 0, s>>>(c);       \
-    else if (nt == 512) k_compact<VPR, 1, 512, 4><<<units, 512, 0, s>>>(c);       \
-    else k_compact<VPR, 1, 1024, 2><<<units, 1024, 0, s>>>(c);                    \
+  const bool hf = (c.flags & ZPC_F_GLOBAL_SCORE) != 0;   // NEXT-2: F rows move with K/V
+  // the index chain a chunk ahead (compact_dev.h) except for 256-wide CTAs over large blocks. A/B on one B200,
+  // compact ms old / index-ahead by CTA width 128 / 256 / 512 / 1024:
+  //   qwen7b (b = 16, 7168 units):        2.63 / 2.60, 2.54 / 2.48, 2.64 / 2.46, -
+  //   paper_op 4 requests (b = 256):      0.480 / 0.483, 0.396 / 0.437, 0.417 / 0.406, 0.437 / 0.413
+  //   paper_op 1 request (b = 256):       -, 0.193 / 0.178, 0.140 / 0.135, 0.114 / 0.111
+  const bool ahead = !(c.b >= 128 && nt == 256);
+#define ZPC_COMPACT_NT(VPR, HF)                                                                   \
+  if (nt == 128) k_compact<VPR, 1, 128, 16, HF, true><<<units, 128, 0, s>>>(c);                  \
+  else if (nt == 256 && ahead) k_compact<VPR, 1, 256, 8, HF, true><<<units, 256, 0, s>>>(c);     \
+  else if (nt == 256) k_compact<VPR, 1, 256, 8, HF, false><<<units, 256, 0, s>>>(c);             \
+  else if (nt == 512) k_compact<VPR, 1, 512, 4, HF, true><<<units, 512, 0, s>>>(c);              \
+  else k_compact<VPR, 1, 1024, 2, HF, true><<<units, 1024, 0, s>>>(c);
+#define ZPC_COMPACT_CASE(VPR)                                                             \
+  case VPR:                                                                              \
+    if (hf) { ZPC_COMPACT_NT(VPR, true) } else { ZPC_COMPACT_NT(VPR, false) }            \
     break;
   switch (vpr) {
     ZPC_COMPACT_CASE(8)
@@ -60,6 +70,7 @@ cudaError_t launch_compact(const Call& c, cudaStream_t s) {
     default: return cudaErrorInvalidValue;
   }
 #undef ZPC_COMPACT_CASE
+#undef ZPC_COMPACT_NT
   return cudaGetLastError();
 }
 
