@@ -25,8 +25,13 @@ namespace zpc {
 namespace {
 
 constexpr int kWarps = 8;            // warps per CTA (k_red_mma)
-constexpr int kBlocksPerWarp = 8;    // consecutive blocks per warp (the next block's rows are
-                                     // prefetched into registers while the current one is computed)
+#ifndef ZPC_RED_BPW
+// consecutive blocks per warp (the next block's rows are prefetched into registers while the current one is
+// computed; the warp's block ids are read once). qwen7b --redundancy, k_red_mma ms at 8 / 16 / 32: 2.69 / 2.62 /
+// 2.59 (0.87 / 0.89 / 0.90 of HBM): fewer warp prologues (first fetch not overlapped)
+#define ZPC_RED_BPW 32
+#endif
+constexpr int kBlocksPerWarp = ZPC_RED_BPW;
 
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& a0, uint32_t& a1, uint32_t& a2, uint32_t& a3) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
@@ -69,8 +74,11 @@ __global__ void __launch_bounds__(kWarps * 32) k_red_mma(Call c) {
   constexpr int NV = 16 * CPR / 32;                 // 16-B vectors per lane per block
   const int jb_first = (blockIdx.y * kWarps + warp) * kBlocksPerWarp;
   int4 pre[NV];
+  // the warp's block ids in one read (lane k holds block jb_first + k), so no fetch waits on a table read
+  static_assert(kBlocksPerWarp <= 32, "one block id per lane");
+  const int myblk = (lane < kBlocksPerWarp && jb_first + lane < nb) ? table[jb_first + lane] : 0;
   auto fetch = [&](int jb) {                        // this lane's share of block jb's 16 rows
-    const int blk = table[jb];
+    const int blk = __shfl_sync(0xffffffffu, myblk, jb - jb_first);
     ZPC_CHECK(blk >= 0 && blk < c.N_total);
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
