@@ -73,7 +73,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   }
 }
 // epilogue waiters that share an SMSP with working warps (k_score_coop's pass-1 / pass-2 warps): try_wait
-// without a suspend-time hint in a lean loop -- a 32-bit poll counter is the hang detector (2^28 polls, seconds)
+// without a suspend-time hint in a lean loop -- a 32-bit poll counter is the hang detector (2^22 polls, ~16 s)
 // instead of a 64-bit counter and a %globaltimer branch per poll. Measured (A/B on one B200): k_score_coop
 // qwen7b 7.53 -> 7.42 ms, k_score_tc --lse-input 3.60 -> 3.53, k_score_ovl llama8b 11.96 -> 11.92; k_score_res
 // paper_op 0.1758 -> 0.1765 (kept on mbar_wait); the same loop for every wait of every kernel 7.75 -> 9.07 ms
@@ -88,7 +88,7 @@ __device__ __forceinline__ void mbar_wait_lean(uint32_t bar, uint32_t parity) {
         : "r"(bar), "r"(parity)
         : "memory");
     if (done) return;
-    if (n == (1u << 28)) wait_trap(bar, parity);
+    if (n == (1u << 22)) wait_trap(bar, parity);   // a failed try_wait suspends ~4 us (scripts/trywait_probe.cu): ~16 s
   }
 }
 // for waiters off the critical path: back off between polls so they do not flood the issue
