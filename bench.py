@@ -578,6 +578,9 @@ def main():
         d2h = 4 * (R * lay.table_stride + host["new_lens"].numel() + R + lay.N_total + int(w.freed.numel()) + 3) + \
             (4 * lay.N_total if href is not None else 0)
         e2e_ms = 0.0
+        # the pinned host arrays are device-accessible: one gather and one scatter kernel instead of ~17 copies
+        params_h = zipc.zpc_params.from_buffer_copy(params)
+        params_h.flags |= zipc.ZPC_F_HOST_MAPPED
         ge = None
         if args.graph:
             # --graph: the same public call captured once (its host<->device copies become memcpy nodes that read
@@ -586,7 +589,7 @@ def main():
             torch.cuda.synchronize()
             ge = torch.cuda.CUDAGraph()
             with torch.cuda.graph(ge):
-                zipc.zpc_compress_host(desc, params, hb, torch.cuda.current_stream())
+                zipc.zpc_compress_host(desc, params_h, hb, torch.cuda.current_stream())
         for i in range(max(3, args.warmup) + args.steps):
             restore()
             for n in host_live:
@@ -599,7 +602,7 @@ def main():
             if ge is not None:
                 ge.replay()
             else:
-                zipc.zpc_compress_host(desc, params, hb, stream)
+                zipc.zpc_compress_host(desc, params_h, hb, stream)
             b_.record(stream)
             b_.synchronize()
             assert int(host["status"][0]) == 0
@@ -610,7 +613,8 @@ def main():
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "path": ("zpc_compress_host" + (" captured as one CUDA graph (memcpy nodes + kernels, replayed per "
                                                  "step)" if args.graph else "") +
-                        ": block tables, budgets, free stack, ref counts host-resident (pinned); "
+                        ": block tables, budgets, free stack, ref counts host-resident (pinned, read and written in "
+                        "place by one gather and one scatter kernel: ZPC_F_HOST_MAPPED); "
                         "K/V/Q caches device-resident (the paged pool lives in HBM)")}
 
     cpu = None

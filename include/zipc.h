@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define ZPC_ABI_VERSION 5
+#define ZPC_ABI_VERSION 6
 
 /* ---- return / status codes ---- */
 #define ZPC_OK                  0
@@ -111,6 +111,13 @@ extern "C" {
                                  every step hurts Qwen3-8B; the paper pools at the first compression only):
                                  requests with is_compressed[r] != 0 select on the unpooled score. Needs
                                  batch.is_compressed (as ZPC_F_GLOBAL_SCORE does). */
+
+#define ZPC_F_HOST_MAPPED 256u /* zpc_compress_host only: every host array of the batch is device-accessible at its
+                                 host address (page-locked with cudaHostAlloc / cudaHostRegister on a unified-
+                                 address system). The call then stages the inputs with ONE gather kernel and
+                                 returns the outputs with ONE scatter kernel that read / write the host arrays
+                                 directly, instead of one copy per array (a small call is otherwise bound by ~17
+                                 copy latencies). Pageable host memory with this flag faults. Ignored elsewhere. */
 
 /* Pool geometry: K, V [L][N_total][b][h_kv][d], Q [L][M][w][h_q][d].
  * Q row u of slot j holds the query of position T-w+u of the request bound to slot j (R3). */
@@ -259,7 +266,8 @@ int zpc_finalize(const zpc_cache_desc* desc, const zpc_params* params, const zpc
  * memory (pinned for async copies); k_cache, v_cache, q_cache, global_scores and workspace are
  * device memory.
  * The call stages the host inputs into the workspace (H2D), runs zpc_compress, and copies every
- * output back (D2H), all on `stream`. Host buffers must stay alive until the stream is synced.
+ * output back (D2H), all on `stream` (per-array copies, or one gather / one scatter kernel with
+ * ZPC_F_HOST_MAPPED). Host buffers must stay alive until the stream is synced.
  * Workspace must be >= zpc_workspace_bytes_host(...). */
 size_t zpc_workspace_bytes_host(const zpc_cache_desc* desc, const zpc_params* params, int32_t num_requests,
                                 int32_t table_stride, int32_t free_capacity, int32_t freed_capacity);

@@ -1,6 +1,7 @@
 // Host side of the C ABI (include/zipc.h): argument validation, workspace carving, stage
 // orchestration on the caller's stream, and the host-buffer e2e variant. No allocation, no
 // global state, no stream synchronisation.
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 
@@ -163,6 +164,27 @@ int run_score(const Call& c, cudaStream_t s) {
   return cuda_rc(launch_score_cudacore(c, s));
 }
 
+// ZPC_F_HOST_MAPPED: the host arrays are read / written in place by one kernel per direction (int32 words)
+struct HostSeg { const int32_t* src; int32_t* dst; uint32_t words; };
+constexpr int kMaxHostSegs = 12;
+struct HostSegs { HostSeg s[kMaxHostSegs]; int n; };
+__global__ void __launch_bounds__(256) k_host_io(HostSegs g) {
+  const HostSeg sg = g.s[blockIdx.y];
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < sg.words; i += gridDim.x * blockDim.x)
+    sg.dst[i] = sg.src[i];
+}
+cudaError_t host_io(const HostSegs& g, cudaStream_t s) {
+  if (g.n == 0) return cudaSuccess;
+  uint32_t mx = 0;
+  for (int i = 0; i < g.n; ++i) mx = mx > g.s[i].words ? mx : g.s[i].words;
+  const unsigned gx = (unsigned)std::min<uint32_t>(64u, (mx + 255u) / 256u);
+  k_host_io<<<dim3(gx > 0 ? gx : 1u, (unsigned)g.n), 256, 0, s>>>(g);
+  return cudaGetLastError();
+}
+void add_seg(HostSegs& g, const void* src, void* dst, size_t bytes) {
+  if (bytes == 0 || !src || !dst) return;
+  g.s[g.n++] = HostSeg{static_cast<const int32_t*>(src), static_cast<int32_t*>(dst), (uint32_t)(bytes / 4)};
+}
 }  // namespace
 }  // namespace zpc
 
@@ -256,17 +278,35 @@ int zpc_compress_host(const zpc_cache_desc* d, const zpc_params* p, const zpc_ba
   int32_t* freed = reinterpret_cast<int32_t*>(take((size_t)h->freed_capacity * 4));
   int32_t* small = reinterpret_cast<int32_t*>(take(16));
   const cudaMemcpyKind H2D = cudaMemcpyHostToDevice, D2H = cudaMemcpyDeviceToHost;
-  if (R) {
-    cudaMemcpyAsync(q_slots, h->q_slots, (size_t)R * 4, H2D, s);
-    cudaMemcpyAsync(seq_lens, h->seq_lens, (size_t)R * 4, H2D, s);
-    cudaMemcpyAsync(tables, h->block_tables, (size_t)R * h->table_stride * 4, H2D, s);
-    cudaMemcpyAsync(budgets, h->budgets, units * 4, H2D, s);
-    if ((p->flags & (ZPC_F_GLOBAL_SCORE | ZPC_F_POOL_FIRST)) && h->is_compressed)
-      cudaMemcpyAsync(comp, h->is_compressed, (size_t)R * 4, H2D, s);
+  const bool mapped = (p->flags & ZPC_F_HOST_MAPPED) != 0;
+  const bool comp_in = (p->flags & (ZPC_F_GLOBAL_SCORE | ZPC_F_POOL_FIRST)) && h->is_compressed;
+  if (mapped) {
+    HostSegs g;
+    g.n = 0;
+    if (R) {
+      add_seg(g, h->q_slots, q_slots, (size_t)R * 4);
+      add_seg(g, h->seq_lens, seq_lens, (size_t)R * 4);
+      add_seg(g, h->block_tables, tables, (size_t)R * h->table_stride * 4);
+      add_seg(g, h->budgets, budgets, units * 4);
+      if (comp_in) add_seg(g, h->is_compressed, comp, (size_t)R * 4);
+    }
+    if (h->ref_counts) add_seg(g, h->ref_counts, refs, (size_t)d->num_blocks * 4);
+    add_seg(g, h->free_stack, stack, (size_t)h->free_capacity * 4);
+    add_seg(g, h->free_top, small, 4);
+    if (cudaError_t e = host_io(g, s)) return cuda_rc(e);
+  } else {
+    if (R) {
+      cudaMemcpyAsync(q_slots, h->q_slots, (size_t)R * 4, H2D, s);
+      cudaMemcpyAsync(seq_lens, h->seq_lens, (size_t)R * 4, H2D, s);
+      cudaMemcpyAsync(tables, h->block_tables, (size_t)R * h->table_stride * 4, H2D, s);
+      cudaMemcpyAsync(budgets, h->budgets, units * 4, H2D, s);
+      if ((p->flags & (ZPC_F_GLOBAL_SCORE | ZPC_F_POOL_FIRST)) && h->is_compressed)
+        cudaMemcpyAsync(comp, h->is_compressed, (size_t)R * 4, H2D, s);
+    }
+    if (h->ref_counts) cudaMemcpyAsync(refs, h->ref_counts, (size_t)d->num_blocks * 4, H2D, s);
+    cudaMemcpyAsync(stack, h->free_stack, (size_t)h->free_capacity * 4, H2D, s);
+    cudaMemcpyAsync(small, h->free_top, 4, H2D, s);
   }
-  if (h->ref_counts) cudaMemcpyAsync(refs, h->ref_counts, (size_t)d->num_blocks * 4, H2D, s);
-  cudaMemcpyAsync(stack, h->free_stack, (size_t)h->free_capacity * 4, H2D, s);
-  cudaMemcpyAsync(small, h->free_top, 4, H2D, s);
   zpc_batch dv = *h;
   dv.q_slots = q_slots; dv.seq_lens = seq_lens; dv.block_tables = tables; dv.budgets = budgets;
   dv.new_lens = new_lens; dv.new_num_blocks = nnb; dv.ref_counts = h->ref_counts ? refs : nullptr;
@@ -275,6 +315,22 @@ int zpc_compress_host(const zpc_cache_desc* d, const zpc_params* p, const zpc_ba
   dv.is_compressed = h->is_compressed ? comp : nullptr;   // global_scores (F), window_lse: device, like K/V/Q
   int rc = zpc_compress(d, p, &dv, stream);
   if (rc != ZPC_OK) return rc;
+  if (mapped) {
+    HostSegs g;
+    g.n = 0;
+    if (R) {
+      add_seg(g, tables, h->block_tables, (size_t)R * h->table_stride * 4);
+      add_seg(g, new_lens, h->new_lens, units * 4);
+      add_seg(g, nnb, h->new_num_blocks, (size_t)R * 4);
+    }
+    if (h->ref_counts) add_seg(g, refs, h->ref_counts, (size_t)d->num_blocks * 4);
+    add_seg(g, stack, h->free_stack, (size_t)h->free_capacity * 4);
+    add_seg(g, freed, h->freed_blocks, (size_t)h->freed_capacity * 4);
+    add_seg(g, small, h->free_top, 4);
+    add_seg(g, small + 1, h->num_freed, 4);
+    add_seg(g, small + 2, h->status, 4);
+    return cuda_rc(host_io(g, s));
+  }
   if (R) {
     cudaMemcpyAsync(h->block_tables, tables, (size_t)R * h->table_stride * 4, D2H, s);
     cudaMemcpyAsync(h->new_lens, new_lens, units * 4, D2H, s);

@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 # ZPC_LIB: an alternative build of the same library (A/B timing of two builds on one GPU box)
 LIB_PATH = os.environ.get("ZPC_LIB") or os.path.join(HERE, "lib", "libzipc.so")
 
-ABI_VERSION = 5  # include/zipc.h ZPC_ABI_VERSION
+ABI_VERSION = 6  # include/zipc.h ZPC_ABI_VERSION
 
 ZPC_OK = 0
 ZPC_ERR_INVALID_ARG = -1
@@ -39,6 +39,7 @@ ZPC_F_REDUNDANCY = 16
 ZPC_F_GLOBAL_SCORE = 32
 ZPC_F_LSE_INPUT = 64
 ZPC_F_POOL_FIRST = 128
+ZPC_F_HOST_MAPPED = 256
 
 ZPC_MAX_SEQ_LEN = 262144
 

@@ -25,7 +25,7 @@ def test_library_exports_every_declared_symbol():
     L = zipc.lib()
     for name in header_functions():
         assert hasattr(L, name), name
-    assert zipc.zpc_abi_version() == zipc.ABI_VERSION == 5
+    assert zipc.zpc_abi_version() == zipc.ABI_VERSION == 6
 
 
 def _desc(**kw):

@@ -183,13 +183,17 @@ def test_device_errors_mutate_nothing(cuda_ok, case):
     assert ref.status == expect
 
 
-def test_host_variant_equals_device(cuda_ok):
-    """zpc_compress_host (host bookkeeping, copies inside the call) == zpc_compress."""
+@pytest.mark.parametrize("mapped", [False, True])
+def test_host_variant_equals_device(cuda_ok, mapped):
+    """zpc_compress_host (host bookkeeping, copies inside the call; with ZPC_F_HOST_MAPPED one gather and one
+    scatter kernel on the pinned host arrays) == zpc_compress."""
     hw = make_host_workload(SMALL7B, 9)
     w1 = from_host(hw)
     run_gpu(w1)
     w2 = from_host(hw)
     desc, params = desc_params(w2)
+    if mapped:
+        params.flags |= zipc.ZPC_F_HOST_MAPPED
     R = int(w2.seq_lens.numel())
     pin = lambda t: t.cpu().pin_memory()  # noqa: E731
     host = {k: pin(getattr(w2, k)) for k in ("q_slots", "seq_lens", "tables", "budgets", "new_lens",
