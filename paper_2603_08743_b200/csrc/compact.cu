@@ -53,6 +53,9 @@ cudaError_t launch_compact(const Call& c, cudaStream_t s) {
   //   paper_op 4 requests (b = 256):      0.480 / 0.483, 0.396 / 0.437, 0.417 / 0.406, 0.437 / 0.413
   //   paper_op 1 request (b = 256):       -, 0.193 / 0.178, 0.140 / 0.135, 0.114 / 0.111
   const bool ahead = !(c.b >= 128 && nt == 256);
+  // __launch_bounds__ keeps 2048 threads per SM (32 registers; 12-84 B of spills, L1-resident). 1536 threads per
+  // SM without most spills (40 registers) measured slower: qwen7b 2.48 -> 2.54 ms, paper_op 0.395 -> 0.499,
+  // llama8b 1.48 -> 1.50
 #define ZPC_COMPACT_NT(VPR, HF)                                                                   \
   if (nt == 128) k_compact<VPR, 1, 128, 16, HF, true><<<units, 128, 0, s>>>(c);                  \
   else if (nt == 256 && ahead) k_compact<VPR, 1, 256, 8, HF, true><<<units, 256, 0, s>>>(c);     \
