@@ -218,6 +218,48 @@ def test_host_variant_equals_device(cuda_ok, mapped):
     assert torch.equal(w1.new_lens.cpu(), host["new_lens"])
 
 
+@pytest.mark.parametrize("mapped", [False, True])
+def test_host_variant_prefix(cuda_ok, mapped):
+    """zpc_compress_host with shared-prefix ref counts: fresh pops, freed shared blocks and the
+    ref-count updates come back to the host arrays identical to the device-resident call, with per-array copies
+    or with the ZPC_F_HOST_MAPPED gather / scatter kernels."""
+    cfg = scaled(CONFIGS["prefix"], L=2, h_kv=2, h_q=14, n_max=9, seq_lens=[400] * 3, prefix_tokens=160,
+                 budget=128, wave=0, free_slack=4)
+    hw = make_host_workload(cfg, 12)
+    w1 = from_host(hw)
+    run_gpu(w1)
+    w2 = from_host(hw)
+    desc, params = desc_params(w2)
+    assert params.flags & zipc.ZPC_F_PREFIX
+    if mapped:
+        params.flags |= zipc.ZPC_F_HOST_MAPPED
+    R = int(w2.seq_lens.numel())
+    pin = lambda t: t.cpu().pin_memory()  # noqa: E731
+    host = {k: pin(getattr(w2, k)) for k in ("q_slots", "seq_lens", "tables", "budgets", "new_lens",
+                                            "new_num_blocks", "ref_counts", "free_stack", "free_top", "freed",
+                                            "num_freed", "status")}
+    need = zipc.zpc_workspace_bytes_host(desc, params, R, host["tables"].shape[1], host["free_stack"].numel(),
+                                         host["freed"].numel())
+    ws = torch.empty(need, dtype=torch.uint8, device="cuda")
+    b = zipc.make_batch(k_cache=w2.k, v_cache=w2.v, q_cache=w2.q, q_slots=host["q_slots"],
+                        seq_lens=host["seq_lens"], block_tables=host["tables"], budgets=host["budgets"],
+                        new_lens=host["new_lens"], new_num_blocks=host["new_num_blocks"], ref_counts=host["ref_counts"],
+                        free_stack=host["free_stack"], free_top=host["free_top"], freed_blocks=host["freed"],
+                        num_freed=host["num_freed"], workspace=ws, status=host["status"])
+    zipc.zpc_compress_host(desc, params, b)
+    torch.cuda.synchronize()
+    assert int(host["status"][0]) == 0
+    assert torch.equal(w1.k.cpu(), w2.k.cpu()) and torch.equal(w1.v.cpu(), w2.v.cpu())
+    assert torch.equal(w1.tables.cpu(), host["tables"])
+    assert torch.equal(w1.ref_counts.cpu(), host["ref_counts"])
+    assert torch.equal(w1.free_stack.cpu(), host["free_stack"]) and int(w1.free_top.item()) == int(host["free_top"][0])
+    n = int(host["num_freed"][0])
+    assert n == int(w1.num_freed.item())
+    assert torch.equal(w1.freed.cpu()[:n], host["freed"][:n])
+    assert torch.equal(w1.new_lens.cpu(), host["new_lens"])
+    assert torch.equal(w1.new_num_blocks.cpu(), host["new_num_blocks"])
+
+
 def test_deterministic(cuda_ok):
     hw = make_host_workload(SMALL7B, 10)
     outs = []
