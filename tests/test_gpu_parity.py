@@ -74,6 +74,17 @@ def test_prefix_small(cuda_ok):
         _run(cfg, seed=6)
 
 
+@pytest.mark.parametrize("kind", ["plain", "prefix"])
+def test_single_request(cuda_ok, kind):
+    """R = 1 takes the single-CTA plan / finalize kernels (k_plan_small, k_finalize_small)."""
+    if kind == "plain":
+        cfg = scaled(CONFIGS["qwen32b"], L=2, h_kv=2, h_q=10, d=64, n_max=6, seq_lens=[333], budget=80, wave=0)
+    else:
+        cfg = scaled(CONFIGS["prefix"], L=2, h_kv=2, h_q=14, n_max=9, seq_lens=[400], prefix_tokens=160,
+                     budget=128, wave=0, free_slack=4)
+    _run(cfg, seed=13)
+
+
 @pytest.mark.parametrize("flags", [0, zipc.ZPC_F_SCORE_CUDACORE])
 def test_paper_operating_point_shape(cuda_ok, flags):
     """NEXT-3: b = 256, w = 16, N_max = 9 with the Qwen3-8B head shape (G = 4), ragged T
