@@ -662,9 +662,12 @@ cudaError_t launch_res(const Call& c, cudaStream_t s) {
 template <int G, int W>
 cudaError_t launch_res_g(const Call& c, cudaStream_t s, bool* used) {
   using K = CfgR<G, W, 128, 8>;   // (NS does not depend on C)
-  // two units (one per epilogue group) resident at once: ceil(tiles / C) <= NS / 2. Among the cluster sizes
-  // that fit, the one with the least work per cluster: (units per cluster) x (tiles of the busiest rank)
-  // (T = 2304: 18 tiles -> C = 6, three tiles on every rank; C = 8 would leave 2 or 3)
+  // a unit's slice must fit a rank's slot ring: ceil(tiles / C) <= NS (with <= NS / 2 the two epilogue groups'
+  // units are resident at once; above it the second unit's MMAs wait for slots, no deadlock: a unit's exchange
+  // never waits on a later unit). Among the sizes that fit, the least work per cluster, counting a unit's fixed
+  // cost (exchange, pipeline fill) as two tiles: (units per cluster) x (tiles of the busiest rank + 2).
+  // Measured at T = 2304 (18 tiles), score ms for C = 4 / 6 / 8: 1 request 0.057 / 0.059 / 0.076, 4 requests
+  // 0.180 / 0.184 / 0.255 -> C = 4 (all 148 SMs, 5 tiles per rank)
   const int npt = (c.max_seq_len + kTile - 1) / kTile;
   const int units = c.R * c.L * c.h_kv;
   int dev = 0, sms = 148;
@@ -674,11 +677,14 @@ cudaError_t launch_res_g(const Call& c, cudaStream_t s, bool* used) {
   long long best_cost = 0;
   for (int cs : {4, 6, 8}) {
     const int per_rank = (npt + cs - 1) / cs;
-    if (per_rank > K::NS / 2) continue;
+    if (per_rank > K::NS) continue;
     const int ncl = std::max(1, std::min(units, sms / cs));
-    const long long cost = (long long)((units + ncl - 1) / ncl) * per_rank;
+    const long long cost = (long long)((units + ncl - 1) / ncl) * (per_rank + 2);
     if (best == 0 || cost < best_cost) { best = cs; best_cost = cost; }
   }
+#ifdef ZPC_TUNING
+  if (const char* e = getenv("ZPC_RES_C")) best = atoi(e);   // A/B: cluster size 4 / 6 / 8
+#endif
   *used = true;
   switch (best) {
     case 4: return launch_res<G, W, 128, 4>(c, s);
